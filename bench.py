@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""MoE-layer fwd+bwd throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1.3b|2.7b|6.7b] [--vanilla]
+
+A step = one moe_forward + moe_backward through the C ABI (every §8(a) row)
+over one batch of synthetic tokens. N = 1 runs BASELINE configs[1] (1.3B-shaped
+layer, 16k tokens/GPU). N > 1 (torchrun, one process per GPU, NCCL) runs the
+same per-GPU workload expert-parallel over N GPUs (E = 16 experts sharded,
+16k tokens per GPU: weak scaling) unless --config picks the 2.7B / 6.7B
+configs. Timing: W warm-up steps, then K steps between barrier +
+synchronize, CUDA events on the launching stream, max over ranks. The working
+set (>1 GB of expert weights per step) exceeds the 126 MB L2, so no flush.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE_SEED = 230513525
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default=None, choices=[None, "1.3b", "2.7b", "6.7b"])
+    p.add_argument("--vanilla", action="store_true", help="disable DTD (G_tensor > 1 configs)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def workload(args, world):
+    """(name, tokens/group, H, F, E, G_t, G_ep)."""
+    cfg = args.config or "1.3b"
+    if cfg == "1.3b":
+        return ("1.3b-ep%d" % world if world > 1 else "1.3b", 16384, 2048, 8192, 16, 1, world)
+    if cfg == "2.7b":
+        return ("2.7b-ep%d" % world, 16384, 2560, 10240, 32, 1, world)
+    gt = 2 if world >= 2 else 1
+    return ("6.7b-tp%dep%d" % (gt, world // gt), 16384, 4096, 16384, 16, gt, world // gt)
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+               0x100: "display_clock", 0x10: "sync_boost"}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                mask = int(parts[3], 16)
+            except ValueError:
+                continue
+            for bit, name in self.REASONS.items():
+                if mask & bit:
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_step(shape_t, sample_tokens, state):
+    """One oracle fwd+bwd on a bounded token sample (same shapes; C scaled with T)."""
+    from oracle import moe_oracle as O
+    xs, dys, wg, w1, w2 = state
+    t0 = time.perf_counter()
+    O.layer(xs, dys, wg, w1, w2, 1.0, 1)
+    return time.perf_counter() - t0
+
+
+def oracle_state(H, F, E, tokens):
+    from oracle import moe_oracle as O
+    from paper_2305_13525_b200 import synth
+    shape = synth.LayerShape("bench", tokens, H, F, E)
+    x = O.decode_bf16(synth.make_x(shape, 0, tokens))
+    dy = O.decode_bf16(synth.make_dy(shape, 0, tokens))
+    wg = synth.make_wg(shape).astype(np.float64)
+    w1, w2 = synth.make_experts(shape)
+    return ([x], [dy], wg, O.decode_bf16(w1), O.decode_bf16(w2))
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info), default=1)
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_cpu_baseline(H, F, E, sample_tokens=256, budget_s=20.0):
+    state = oracle_state(H, F, E, sample_tokens)
+    cpu_oracle_step(None, sample_tokens, state)  # warm
+    times = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and len(times) < 50:
+        times.append(cpu_oracle_step(None, sample_tokens, state))
+    dt = float(np.mean(times))
+    return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"oracle fwd+bwd on {sample_tokens} tokens (H={H}, F={F}, E={E}, cf=1.0), "
+                      f"mean of {len(times)} runs, float64 numpy"}
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    name, T, H, F, E, gt, gep = workload(args, 1)
+    sample = 256
+    state = oracle_state(H, F, E, sample)
+    for _ in range(args.warmup):
+        cpu_oracle_step(None, sample, state)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_oracle_step(None, sample, state)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    v = sample / dt
+    out = {"metric": "MoE-layer fwd+bwd tokens/s", "value": v, "unit": "tokens/s", "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": name, "tokens_sample": sample, "hidden": H,
+                                           "ffn": F, "experts": E},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                            "sample": f"{sample} tokens per step of the {name} layer"},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    from paper_2305_13525_b200 import MOE_F_STATS, MOE_F_TIMING, MoEConfig, MoELayer, lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    lib()  # fail loudly if the CUDA library is missing
+
+    name, T, H, F, E, gt, gep = workload(args, world)
+    dtd = not args.vanilla
+    cfg = MoEConfig(T, H, F, E, 1.0, gt, gep, dtd, MOE_F_STATS | MOE_F_TIMING)
+    layer = MoELayer(cfg, world, rank, dev)
+    L = layer.layout
+    El, Fl = L["experts_local"], L["ffn_local"]
+    group = L["d"] * gep + L["ep"]
+
+    def gen(shape, seed, scale=1.0, dtype=torch.bfloat16):
+        g = torch.Generator(device=dev).manual_seed(seed)
+        return (torch.randn(shape, generator=g, device=dev) * scale).to(dtype)
+
+    x = gen((T, H), BASE_SEED + group)
+    dy = gen((T, H), BASE_SEED + 3000 + group)
+    wg = gen((H, E), BASE_SEED + 1000, 1 / math.sqrt(H), torch.float32)
+    w1 = gen((El, Fl, H), BASE_SEED + 2000 + rank, 1 / math.sqrt(H))
+    w2 = gen((El, H, Fl), BASE_SEED + 5000 + rank, 1 / math.sqrt(F))
+    y = torch.empty_like(x)
+    saved = layer.new_saved()
+    grads = (torch.empty_like(x), torch.empty_like(wg), torch.empty_like(w1), torch.empty_like(w2))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        layer.moe_forward(x, wg, w1, w2, y=y, saved=saved)
+        layer.moe_backward(dy, saved, x, wg, w1, w2, out=grads)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    layer.moe_stats()          # resolve warm-up events
+    layer.moe_stats_reset()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    st = layer.moe_stats()
+    ms_t = torch.tensor([ms], device=dev)
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    S = world // gt
+    tokens_per_step = S * T
+    value = tokens_per_step / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel class: the tcgen05 expert GEMMs
+    rt = layer.moe_routing(saved)
+    kept_local = int(rt["count"].sum().item())  # this group's kept tokens
+    kept_t = torch.tensor([kept_local], device=dev, dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(kept_t)
+    kept_all = float(kept_t.item()) / gt  # kept tokens over all token groups (TP ranks duplicate)
+    # algorithmic GEMM FLOPs per rank per step: 12 * H * F_l per kept token routed to this rank's
+    # experts; on average kept_all / G_ep tokens reach each EP rank (every TP rank holds F/G_t).
+    gemm_flops_step = 12.0 * H * Fl * kept_all / gep
+    gemm_ms = st["kernel_ms"]["gemm"] / args.steps
+    peaks, peak_src = load_peaks()
+    achieved = gemm_flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    launches_per_step = sum(st["kernel_launches"].values()) / args.steps
+    gemm_launch_ms = gemm_ms / 6.0
+    roofline = {"bound": "tensor", "kernel": "gemm_kernel (tcgen05, 6 launches/step)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "peak_kind": f"{peak_src} bf16 sustained (kernel inside a long step)",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "ms_per_launch": gemm_launch_ms, "share_of_step": gemm_ms / ms}
+    per_class = {k: v / args.steps for k, v in st["kernel_ms"].items()}
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty_like(x, device="cpu").pin_memory().copy_(x)
+        hdy = torch.empty_like(dy, device="cpu").pin_memory().copy_(dy)
+        hy = torch.empty_like(y, device="cpu").pin_memory()
+        hdx = torch.empty_like(x, device="cpu").pin_memory()
+        xd, dyd = torch.empty_like(x), torch.empty_like(dy)
+
+        def e2e_step():
+            xd.copy_(hx, non_blocking=True)
+            dyd.copy_(hdy, non_blocking=True)
+            layer.moe_forward(xd, wg, w1, w2, y=y, saved=saved)
+            layer.moe_backward(dyd, saved, xd, wg, w1, w2, out=grads)
+            hy.copy_(y, non_blocking=True)
+            hdx.copy_(grads[0], non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        barrier()
+        n_e2e = max(5, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        ms_e = torch.tensor([e0.elapsed_time(e1) / n_e2e], device=dev)
+        if dist is not None:
+            dist.all_reduce(ms_e, op=dist.ReduceOp.MAX)
+        nb = x.numel() * 2
+        e2e = {"value": tokens_per_step / (float(ms_e.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
+               "what": "pinned host x, dy -> device; moe_forward + moe_backward; y, dx -> host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(H, F, E)
+
+    if rank == 0:
+        out = {"metric": "MoE-layer fwd+bwd tokens/s", "value": value, "unit": "tokens/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+               "data": "synthetic (x, dy ~ N(0,1); Wg ~ N(0,1/H); W1 ~ N(0,1/H); W2 ~ N(0,1/F))",
+               "config": {"workload": name, "tokens_per_group": T, "hidden": H, "ffn": F, "experts": E,
+                          "capacity_factor": 1.0, "g_tensor": gt, "g_expert": gep,
+                          "dtd": bool(dtd and gt > 1), "token_groups": S,
+                          "l2": "no flush: >1 GB expert weights + activations per step exceed 126 MB L2"},
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": int(round(launches_per_step * args.steps)),
+               "launches_per_step": launches_per_step, "clocks": clk,
+               "kernel_ms_per_step": per_class,
+               "dropped_tokens": st["dropped_tokens"], "tie_tokens": st["tie_tokens"],
+               "collectives": {"calls": st["calls"], "wire_bytes": st["wire_bytes"]}}
+        if world > 1:
+            a2a_ms = per_class["comm"]
+            out["comm_ms_per_step"] = a2a_ms
+        print(json.dumps(out), flush=True)
+    layer.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+/*
+ * moe.h — C ABI of the B200-native MoE layer (arXiv 2305.13525 hot path).
+ *
+ * The layer: top-1 gating with expert capacity, the dispatch permutation,
+ * the expert-parallel all-to-all with Duplicate Token Dropping (DTD,
+ * PAPER.md:1116-1163), the per-expert FFN (tensor-parallel over G_tensor,
+ * PAPER.md:119-122) and the weighted combine. "Following previous work ...
+ * every alternate layer has expert feedforward modules";
+ * the gate itself is defined by BASELINE.json north_star and DESIGN.md
+ * readings R1-R8 (the paper never specifies it).
+ *
+ * Process model: one process per GPU. Rank r = (d*G_expert + ep)*G_tensor + t
+ * (R17): TP group = ranks sharing (d, ep); EP group = ranks sharing
+ * (d, t). A TP group holds one token group of T tokens, replicated on its
+ * G_tensor ranks (the Megatron all-reduce duplication).
+ * Rank (d, ep, t) owns experts [ep*E_l, (ep+1)*E_l), E_l = E/G_expert, and
+ * for each the F-slice [t*F/G_t, (t+1)*F/G_t): rows of W1 [F,H], columns of
+ * W2 [H,F] (Megatron column/row split).
+ *
+ * Conventions for every call:
+ *  - Tensor pointers are caller-owned CUDA device pointers unless stated;
+ *    the library never allocates, frees or retains them past the call.
+ *    bf16 tensors are passed as void* (2-byte elements, row-major).
+ *  - Work is enqueued asynchronously on the given stream (NCCL calls too);
+ *    ordering is stream order. Outputs are overwritten, never accumulated.
+ *  - Every call returns a moe_status; nothing throws or aborts across the
+ *    ABI. Validation happens before anything is enqueued. A CUDA/NCCL
+ *    failure poisons the ctx: later calls return MOE_ERR_STATE.
+ *    moe_last_error_detail() gives a thread-local message for the last error.
+ *  - A ctx is not thread-safe.
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_ARG = 1,         /* null pointer / out-of-range scalar                   */
+  MOE_ERR_SHAPE = 2,       /* divisibility / size constraint violated              */
+  MOE_ERR_ALIGN = 3,       /* pointer not 16-byte aligned (TMA / 16B vectors)      */
+  MOE_ERR_STATE = 4,       /* wrong saved blob, poisoned ctx, missing comm         */
+  MOE_ERR_CUDA = 5,        /* CUDA runtime / driver error                          */
+  MOE_ERR_NCCL = 6,        /* NCCL error                                           */
+  MOE_ERR_UNSUPPORTED = 7  /* valid request this build does not implement         */
+} moe_status;
+
+/* moe_config.flags */
+#define MOE_F_STATS 1u            /* keep the per-collective byte ledger (moe_stats)        */
+#define MOE_F_FORCED_ROUTING 2u   /* moe_forward takes forced_expert[T] instead of argmax   */
+#define MOE_F_TIMING 4u           /* record CUDA events around every kernel class (moe_stats) */
+
+/* Layer configuration. Identical on every rank of the job.
+ * Constraints (checked, MOE_ERR_SHAPE otherwise):
+ *   tokens >= 1; hidden % 64 == 0; experts in [1, 64];
+ *   ffn % g_tensor == 0 and (ffn / g_tensor) % 64 == 0;
+ *   experts % g_expert == 0; world == g_tensor * g_expert * G_data (G_data >= 1);
+ *   capacity_factor > 0. */
+typedef struct {
+  int64_t tokens;          /* T: tokens per TP group, identical on its G_tensor ranks */
+  int32_t hidden;          /* H                                                        */
+  int32_t ffn;             /* F, unsharded                                             */
+  int32_t experts;         /* E, global                                                */
+  float capacity_factor;   /* cf                                                       */
+  int32_t g_tensor;        /* G_tensor                                  */
+  int32_t g_expert;        /* G_expert                                */
+  int32_t dtd;             /* 0 = vanilla (AllReduce + full all-to-all), 1 = DTD       */
+  uint32_t flags;          /* MOE_F_*                                                  */
+} moe_config;
+
+/* Per-rank derived layout (host-only; no GPU needed). */
+typedef struct {
+  int32_t world, rank;
+  int32_t d, ep, t;        /* rank coordinates                                         */
+  int32_t experts_local;   /* E_l = E / G_expert                                       */
+  int32_t ffn_local;       /* F_l = F / G_tensor                                       */
+  int64_t capacity;        /* C = ceil(cf*T/E) rounded up to a multiple of G_tensor, >= 1 (R2) */
+  int64_t slot_slice;      /* C_s = C / G_tensor: one DTD slot slice                   */
+  int64_t rows_per_expert; /* R = G_expert * C: GEMM rows of one local expert          */
+  int32_t token_groups;    /* S = world / G_tensor                                     */
+} moe_layout;
+
+typedef struct moe_ctx moe_ctx;
+
+/* Collective kinds in the ledger. */
+enum { MOE_COLL_A2A = 0, MOE_COLL_ALLGATHER = 1, MOE_COLL_REDUCESCATTER = 2,
+       MOE_COLL_ALLREDUCE = 3, MOE_COLL_KINDS = 4 };
+
+/* One collective call of the forward+backward schedule (host-side plan).
+ * wire_bytes: bytes this rank puts on NVLink for the call under the
+ * lower-bound convention of PAPER.md:612-622 — all-to-all: bytes sent to
+ * other ranks; all-gather / reduce-scatter: (s-1)/s x the full buffer;
+ * all-reduce: 2(s-1)/s x the buffer (s = group size). */
+typedef struct {
+  int32_t kind;            /* MOE_COLL_*                                               */
+  int32_t pass;            /* 0 = forward, 1 = backward                                */
+  int32_t step;            /* SURVEY §8(a) step id: 4,5,8,9,10 (F) / 2,3,7,8,9 (B)      */
+  int32_t group_size;      /* s                                                        */
+  int64_t buffer_bytes;    /* full buffer (a2a: send buffer incl. self chunk)          */
+  int64_t wire_bytes;
+} moe_collective;
+
+/* Kernel classes of the ledger. */
+enum { MOE_K_ROUTE = 0,       /* F1 gate + F2 slot scan                 */
+       MOE_K_DISPATCH = 1,    /* F3                                     */
+       MOE_K_GEMM = 2,        /* F6 F7 B4 B5 B6 (tcgen05 expert GEMMs)  */
+       MOE_K_COMBINE = 3,     /* F11                                    */
+       MOE_K_COMBINE_BWD = 4, /* B1                                     */
+       MOE_K_GATE_BWD = 5,    /* B10                                    */
+       MOE_K_COMM = 6,        /* NCCL collectives + self-chunk copies   */
+       MOE_K_CLASSES = 7 };
+
+typedef struct {
+  int64_t calls[MOE_COLL_KINDS];
+  int64_t wire_bytes[MOE_COLL_KINDS];
+  int64_t forward_calls, backward_calls;
+  int64_t dropped_tokens;  /* last forward: tokens beyond capacity (this group)       */
+  int64_t tie_tokens;      /* last forward: top-2 gap < 1e-6 (logged ties)            */
+  int32_t nccl_async_error;/* ncclCommGetAsyncError of the last check (0 = none)      */
+  int64_t kernel_launches[MOE_K_CLASSES]; /* CUDA kernels this library launched, per class */
+  double kernel_ms[MOE_K_CLASSES];        /* MOE_F_TIMING: summed CUDA-event time per class */
+} moe_stats;
+
+/* ---------------- host-only planning (no GPU, no ctx) ---------------- */
+
+/* Validates cfg for (world, rank) and fills the derived layout. */
+moe_status moe_plan_layout(const moe_config* cfg, int world, int rank, moe_layout* out);
+
+/* Sizes of the caller-allocated buffers: saved (one forward's stash for its
+ * backward: routing record, expert inputs X, Hpre, A = gelu(Hpre), combine
+ * source O) and scratch (transient; may be shared by consecutive calls on one
+ * stream). Both must be 256-byte aligned device memory. */
+moe_status moe_plan_bytes(const moe_config* cfg, int world, int rank,
+                          size_t* saved_bytes, size_t* scratch_bytes);
+
+/* The collective schedule of one forward+backward on this rank, in issue
+ * order (the ledger moe_forward/moe_backward actually follow). If out is
+ * NULL or cap is too small only *n is written. */
+moe_status moe_plan_collectives(const moe_config* cfg, int world, int rank,
+                                moe_collective* out, int cap, int* n);
+
+/* ---------------- context ---------------- */
+
+/* Rank 0 creates the NCCL unique id; the caller broadcasts the 128 bytes
+ * (e.g. with torch.distributed) before moe_create. */
+moe_status moe_get_unique_id(uint8_t uid[128]);
+
+/* Collective over the world when world > 1 (ncclCommInitRank + ncclCommSplit
+ * into the TP and EP communicators); uid is ignored when world == 1. The CUDA
+ * device must already be current. scratch/scratch_bytes: caller-owned device
+ * buffer of at least moe_plan_bytes' scratch size, used by every call on this
+ * ctx. */
+moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, int rank,
+                      void* scratch, size_t scratch_bytes, moe_ctx** out);
+
+/* Forward.
+ *   x      bf16 [T, H]            tokens of this rank's TP group
+ *   wg     fp32 [H, E]            gate weight (replicated)
+ *   w1     bf16 [E_l, F_l, H]     this rank's W1 shards
+ *   w2     bf16 [E_l, H, F_l]     this rank's W2 shards
+ *   y      bf16 [T, H]            output: p_t * FFN_{e_t}(x_t), 0 for dropped tokens
+ *   saved  device blob of moe_plan_bytes' saved size (written)
+ *   forced_expert  int32 [T] or NULL; required iff MOE_F_FORCED_ROUTING. */
+moe_status moe_forward(moe_ctx* ctx, const void* x, const float* wg, const void* w1,
+                       const void* w2, void* y, void* saved, const int32_t* forced_expert,
+                       void* stream);
+
+/* Backward. dy bf16 [T, H]; saved from this ctx's
+ * forward on the same x/wg/w1/w2. Outputs (overwritten):
+ *   dx  bf16 [T, H]; dwg fp32 [H, E] (this token group's gradient);
+ *   dw1 bf16 [E_l, F_l, H]; dw2 bf16 [E_l, H, F_l] (summed over every token
+ *   routed to the shard within its EP group; no data-parallel reduction). */
+moe_status moe_backward(moe_ctx* ctx, const void* dy, const void* saved, const void* x,
+                        const float* wg, const void* w1, const void* w2, void* dx,
+                        float* dwg, void* dw1, void* dw2, void* stream);
+
+/* Copies the routing record of a saved blob (device -> device, async).
+ * expert/slot int32 [T] (slot -1 = dropped), prob/gap fp32 [T],
+ * count int32 [E] (kept per expert, <= C). Any output may be NULL. */
+moe_status moe_routing(moe_ctx* ctx, const void* saved, int32_t* expert, int32_t* slot,
+                       float* prob, float* gap, int32_t* count, void* stream);
+
+/* Ledger + last-forward routing counters + per-class kernel launches/times;
+ * synchronizes the ctx's last stream. */
+moe_status moe_stats_get(moe_ctx* ctx, moe_stats* out);
+moe_status moe_stats_reset(moe_ctx* ctx);
+
+moe_status moe_destroy(moe_ctx* ctx);
+
+const char* moe_status_string(moe_status s);
+const char* moe_last_error_detail(void);
+
+/* ---------------- diagnostics: the expert GEMM on its own ----------------
+ * D[b] = epilogue(A[b] . B[b]^T) for b < batch, bf16 in, fp32 accumulate in
+ * TMEM (tcgen05), bf16 out. Used by the tests and the GEMM micro-benchmark.
+ *   A: a_mn == 0 -> [batch][M][K] (K-major);  a_mn == 1 -> [batch][K][M]
+ *   B: b_mn == 0 -> [batch][N][K] (K-major);  b_mn == 1 -> [batch][K][N]
+ *   D: [batch][M][N].  M, K >= 1; N % 64 == 0; M, K, N multiples of 8.
+ *   epilogue 0: D = bf16(acc)
+ *   epilogue 1: D = bf16(acc) (Hpre), aux = bf16(gelu_tanh(acc)) [batch][M][N]
+ *   epilogue 2: D = bf16(acc * gelu_tanh'(aux)), aux = Hpre bf16 [batch][M][N] (read)
+ *   impl 0: tcgen05 kernel (the product path); impl 1: plain SIMT reference
+ *   kernel (bring-up cross-check only; never used by moe_forward/backward). */
+moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn,
+                         const void* B, int b_mn, void* D, int epilogue, void* aux,
+                         int impl, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H */

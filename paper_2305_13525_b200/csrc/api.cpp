@@ -1,0 +1,599 @@
+// api.cpp — the C ABI of include/moe.h: context, NCCL communicators, and the
+// per-call step list of SURVEY §8(a) enqueued on the caller's stream.
+//
+// HBM layouts:
+//   slot space   [G_t][E][C_s][H]          dispatch send buffer D, combine source O, dO, dS
+//   expert space [E_l][G_t][G_ep][C_s][H]  expert inputs X, Ypart, dY, dXpart (R = G_ep*C rows / expert)
+// Slot c of expert e sits in slot slice c / C_s, so DTD's "drop"
+// is "dispatch only my slice", its all-gather is an in-place
+// ncclAllGather per local expert over the TP communicator, and AR + drop on the
+// return path is an in-place ncclReduceScatter (R11, R12). Vanilla and
+// DTD feed the expert GEMMs the same rows in the same positions.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/moe.h"
+#include "internal.h"
+#include "plan.h"
+
+using namespace moe;
+
+struct moe_ctx {
+  Dims d;
+  moe_config cfg;
+  SavedLayout sv;
+  ScratchLayout sc;
+  uint8_t* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  ncclComm_t world_comm = nullptr, tp_comm = nullptr, ep_comm = nullptr;
+  bool poisoned = false;
+  moe_stats stats;
+  std::unordered_set<const void*> saved_written;
+  const void* last_saved = nullptr;
+  cudaStream_t last_stream = nullptr;
+  // MOE_F_TIMING: event pairs per kernel class, resolved in moe_stats_get
+  bool timing = false;
+  struct Span { int cls; cudaEvent_t a, b; };
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> pool;
+  ~moe_ctx() {
+    for (auto& s : spans) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+thread_local std::string g_detail;
+
+moe_status fail(moe_status s, const std::string& why) {
+  g_detail = why;
+  return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) {                                                                 \
+      if (ctx) (ctx)->poisoned = true;                                                       \
+      return fail(MOE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));         \
+    }                                                                                        \
+  } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    ncclResult_t _r = (expr);                                                                \
+    if (_r != ncclSuccess) {                                                                 \
+      if (ctx) (ctx)->poisoned = true;                                                       \
+      return fail(MOE_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));         \
+    }                                                                                        \
+  } while (0)
+
+cudaEvent_t take_event(moe_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+// Counts this library's kernel launches per class and, with MOE_F_TIMING,
+// brackets the class's work with CUDA events on the launching stream.
+struct Scope {
+  moe_ctx* c;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  Scope(moe_ctx* c_, int cls_, cudaStream_t st_, int kernels) : c(c_), cls(cls_), st(st_) {
+    c->stats.kernel_launches[cls] += kernels;
+    if (c->timing && (a = take_event(c)) != nullptr) cudaEventRecord(a, st);
+  }
+  ~Scope() {
+    if (!a) return;
+    cudaEvent_t b = take_event(c);
+    if (!b) { c->pool.push_back(a); return; }
+    cudaEventRecord(b, st);
+    c->spans.push_back({cls, a, b});
+  }
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <typename T>
+T* at(void* base, size_t off) { return reinterpret_cast<T*>(static_cast<uint8_t*>(base) + off); }
+template <typename T>
+const T* at(const void* base, size_t off) {
+  return reinterpret_cast<const T*>(static_cast<const uint8_t*>(base) + off);
+}
+
+SlotSpace slot_space(const Dims& d) {
+  SlotSpace s;
+  s.C = d.C; s.Cs = d.Cs; s.G_t = d.Gt; s.E = d.E; s.H = d.H;
+  return s;
+}
+
+void ledger(moe_ctx* c, int kind, int pass, int64_t wire) {
+  c->stats.calls[kind] += 1;
+  c->stats.wire_bytes[kind] += wire;
+  if (pass == 0) c->stats.forward_calls += 1; else c->stats.backward_calls += 1;
+}
+
+// ---- EP exchange between slot space S and expert space X (F4/F9/B2/B8) ----
+// dir 0: S_me(tt, p*E_l+el) -> X_p(el, tt, ep_me);  dir 1: X_me(el, tt, p) -> S_p(tt, ep_me*E_l+el).
+moe_status ep_exchange(moe_ctx* c, int dir, int pass, void* S, void* X, int lo, int hi,
+                       cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t piece = (size_t)d.Cs * d.H;  // elements
+  const size_t pbytes = piece * 2;
+  auto s_at = [&](int tt, int e) { return at<uint8_t>(S, ((size_t)tt * d.E + e) * pbytes); };
+  auto x_at = [&](int el, int tt, int src) {
+    return at<uint8_t>(X, (((size_t)el * d.Gt + tt) * d.Gep + src) * pbytes);
+  };
+  // self pieces: device copies
+  for (int el = 0; el < d.El; ++el)
+    for (int tt = lo; tt < hi; ++tt) {
+      if (dir == 0)
+        CUDA_TRY(c, cudaMemcpyAsync(x_at(el, tt, d.ep), s_at(tt, d.ep * d.El + el), pbytes,
+                                    cudaMemcpyDeviceToDevice, st));
+      else
+        CUDA_TRY(c, cudaMemcpyAsync(s_at(tt, d.ep * d.El + el), x_at(el, tt, d.ep), pbytes,
+                                    cudaMemcpyDeviceToDevice, st));
+    }
+  if (d.Gep == 1) return MOE_OK;
+  NCCL_TRY(c, ncclGroupStart());
+  for (int p = 0; p < d.Gep; ++p) {
+    if (p == d.ep) continue;
+    for (int el = 0; el < d.El; ++el)
+      for (int tt = lo; tt < hi; ++tt) {
+        if (dir == 0) {
+          NCCL_TRY(c, ncclSend(s_at(tt, p * d.El + el), piece, ncclBfloat16, p, c->ep_comm, st));
+          NCCL_TRY(c, ncclRecv(x_at(el, tt, p), piece, ncclBfloat16, p, c->ep_comm, st));
+        } else {
+          NCCL_TRY(c, ncclSend(x_at(el, tt, p), piece, ncclBfloat16, p, c->ep_comm, st));
+          NCCL_TRY(c, ncclRecv(s_at(tt, p * d.El + el), piece, ncclBfloat16, p, c->ep_comm, st));
+        }
+      }
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  ledger(c, MOE_COLL_A2A, pass, (int64_t)(d.Gep - 1) * d.El * (hi - lo) * (int64_t)pbytes);
+  return MOE_OK;
+}
+
+// F5/B3: in-place all-gather of expert space over TP, one call per local expert.
+moe_status ag_expert(moe_ctx* c, int pass, void* X, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t cnt = (size_t)d.Gep * d.Cs * d.H;
+  NCCL_TRY(c, ncclGroupStart());
+  for (int el = 0; el < d.El; ++el) {
+    uint8_t* base = at<uint8_t>(X, (size_t)el * d.R * d.H * 2);
+    NCCL_TRY(c, ncclAllGather(base + (size_t)d.t * cnt * 2, base, cnt, ncclBfloat16, c->tp_comm, st));
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
+  ledger(c, MOE_COLL_ALLGATHER, pass, xe * (d.Gt - 1) / d.Gt);
+  return MOE_OK;
+}
+
+// F8/B7 under DTD: in-place reduce-scatter of expert space over TP (AR + drop = RS).
+moe_status rs_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t cnt = (size_t)d.Gep * d.Cs * d.H;
+  NCCL_TRY(c, ncclGroupStart());
+  for (int el = 0; el < d.El; ++el) {
+    uint8_t* base = at<uint8_t>(Y, (size_t)el * d.R * d.H * 2);
+    NCCL_TRY(c, ncclReduceScatter(base, base + (size_t)d.t * cnt * 2, cnt, ncclBfloat16, ncclSum,
+                                  c->tp_comm, st));
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
+  ledger(c, MOE_COLL_REDUCESCATTER, pass, xe * (d.Gt - 1) / d.Gt);
+  return MOE_OK;
+}
+
+// F8/B7 vanilla: the Megatron all-reduce of the row-parallel partials.
+moe_status ar_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t cnt = (size_t)d.El * d.R * d.H;
+  NCCL_TRY(c, ncclAllReduce(Y, Y, cnt, ncclBfloat16, ncclSum, c->tp_comm, st));
+  ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * (int64_t)cnt * 2 * (d.Gt - 1) / d.Gt);
+  return MOE_OK;
+}
+
+// F10/B9: in-place all-gather of slot space over TP.
+moe_status ag_slot(moe_ctx* c, int pass, void* O, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t cnt = (size_t)d.E * d.Cs * d.H;
+  NCCL_TRY(c, ncclAllGather(at<uint8_t>(O, (size_t)d.t * cnt * 2), O, cnt, ncclBfloat16, c->tp_comm, st));
+  ledger(c, MOE_COLL_ALLGATHER, pass, (int64_t)d.E * d.C * d.H * 2 * (d.Gt - 1) / d.Gt);
+  return MOE_OK;
+}
+
+moe_status gemm(moe_ctx* c, const GemmArgs& g, cudaStream_t st) {
+  const char* why = "";
+  if (c) {
+    Scope sc_(c, MOE_K_GEMM, st, 1);
+    cudaError_t e = gemm_tc(g, st, &why);
+    if (e != cudaSuccess) {
+      c->poisoned = true;
+      return fail(MOE_ERR_CUDA, std::string("expert GEMM: ") + why + " (" + cudaGetErrorString(e) + ")");
+    }
+    return MOE_OK;
+  }
+  cudaError_t e = gemm_tc(g, st, &why);
+  if (e != cudaSuccess) {
+    if (c) c->poisoned = true;
+    return fail(MOE_ERR_CUDA, std::string("expert GEMM: ") + why + " (" + cudaGetErrorString(e) + ")");
+  }
+  return MOE_OK;
+}
+
+#define TRY(expr)                         \
+  do {                                    \
+    moe_status _s = (expr);               \
+    if (_s != MOE_OK) return _s;          \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* moe_status_string(moe_status s) {
+  switch (s) {
+    case MOE_OK: return "MOE_OK";
+    case MOE_ERR_ARG: return "MOE_ERR_ARG";
+    case MOE_ERR_SHAPE: return "MOE_ERR_SHAPE";
+    case MOE_ERR_ALIGN: return "MOE_ERR_ALIGN";
+    case MOE_ERR_STATE: return "MOE_ERR_STATE";
+    case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
+    case MOE_ERR_NCCL: return "MOE_ERR_NCCL";
+    case MOE_ERR_UNSUPPORTED: return "MOE_ERR_UNSUPPORTED";
+  }
+  return "MOE_ERR_UNKNOWN";
+}
+
+const char* moe_last_error_detail(void) { return g_detail.c_str(); }
+
+moe_status moe_plan_layout(const moe_config* cfg, int world, int rank, moe_layout* out) {
+  if (!out) return fail(MOE_ERR_ARG, "null output");
+  Dims d;
+  std::string why;
+  moe_status s = make_dims(cfg, world, rank, &d, &why);
+  if (s != MOE_OK) return fail(s, why);
+  out->world = world; out->rank = rank;
+  out->d = d.d; out->ep = d.ep; out->t = d.t;
+  out->experts_local = d.El; out->ffn_local = d.Fl;
+  out->capacity = d.C; out->slot_slice = d.Cs; out->rows_per_expert = d.R;
+  out->token_groups = d.S;
+  return MOE_OK;
+}
+
+moe_status moe_plan_bytes(const moe_config* cfg, int world, int rank, size_t* saved_bytes,
+                          size_t* scratch_bytes) {
+  Dims d;
+  std::string why;
+  moe_status s = make_dims(cfg, world, rank, &d, &why);
+  if (s != MOE_OK) return fail(s, why);
+  SavedLayout sv;
+  ScratchLayout sc;
+  make_layouts(d, &sv, &sc);
+  if (saved_bytes) *saved_bytes = sv.total;
+  if (scratch_bytes) *scratch_bytes = sc.total;
+  return MOE_OK;
+}
+
+moe_status moe_plan_collectives(const moe_config* cfg, int world, int rank, moe_collective* out,
+                                int cap, int* n) {
+  if (!n) return fail(MOE_ERR_ARG, "null count");
+  Dims d;
+  std::string why;
+  moe_status s = make_dims(cfg, world, rank, &d, &why);
+  if (s != MOE_OK) return fail(s, why);
+  std::vector<moe_collective> v = make_schedule(d);
+  *n = (int)v.size();
+  if (out && cap >= (int)v.size()) std::memcpy(out, v.data(), v.size() * sizeof(moe_collective));
+  return MOE_OK;
+}
+
+moe_status moe_get_unique_id(uint8_t uid[128]) {
+  if (!uid) return fail(MOE_ERR_ARG, "null uid");
+  ncclUniqueId id;
+  NCCL_TRY((moe_ctx*)nullptr, ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(uid, &id, 128);
+  return MOE_OK;
+}
+
+moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, int rank,
+                      void* scratch, size_t scratch_bytes, moe_ctx** out) {
+  if (!out) return fail(MOE_ERR_ARG, "null ctx output");
+  *out = nullptr;
+  Dims d;
+  std::string why;
+  moe_status s = make_dims(cfg, world, rank, &d, &why);
+  if (s != MOE_OK) return fail(s, why);
+  moe_ctx* c = new moe_ctx();
+  c->d = d;
+  c->cfg = *cfg;
+  c->timing = (cfg->flags & MOE_F_TIMING) != 0;
+  make_layouts(d, &c->sv, &c->sc);
+  std::memset(&c->stats, 0, sizeof(c->stats));
+  if (!scratch || scratch_bytes < c->sc.total) {
+    delete c;
+    return fail(MOE_ERR_ARG, "scratch missing or smaller than moe_plan_bytes");
+  }
+  if (reinterpret_cast<uintptr_t>(scratch) & 255) {
+    delete c;
+    return fail(MOE_ERR_ALIGN, "scratch must be 256-byte aligned");
+  }
+  c->scratch = static_cast<uint8_t*>(scratch);
+  c->scratch_bytes = scratch_bytes;
+  if (world > 1) {
+    if (!uid) { delete c; return fail(MOE_ERR_ARG, "uid required when world > 1"); }
+    ncclUniqueId id;
+    std::memcpy(&id, uid, 128);
+    ncclResult_t r = ncclCommInitRank(&c->world_comm, world, id, rank);
+    if (r != ncclSuccess) { delete c; return fail(MOE_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); }
+    r = ncclCommSplit(c->world_comm, d.d * d.Gep + d.ep, d.t, &c->tp_comm, nullptr);
+    if (r == ncclSuccess) r = ncclCommSplit(c->world_comm, d.d * d.Gt + d.t, d.ep, &c->ep_comm, nullptr);
+    if (r != ncclSuccess) {
+      ncclCommDestroy(c->world_comm);
+      delete c;
+      return fail(MOE_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return MOE_OK;
+}
+
+moe_status moe_destroy(moe_ctx* c) {
+  if (!c) return MOE_OK;
+  if (c->tp_comm) ncclCommDestroy(c->tp_comm);
+  if (c->ep_comm) ncclCommDestroy(c->ep_comm);
+  if (c->world_comm) ncclCommDestroy(c->world_comm);
+  delete c;
+  return MOE_OK;
+}
+
+moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w1, const void* w2,
+                       void* y, void* saved, const int32_t* forced_expert, void* stream) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  if (c->poisoned) return fail(MOE_ERR_STATE, "ctx poisoned by an earlier CUDA/NCCL failure");
+  if (!x || !wg || !w1 || !w2 || !y || !saved) return fail(MOE_ERR_ARG, "null tensor pointer");
+  if (c->d.forced != (forced_expert != nullptr))
+    return fail(MOE_ERR_ARG, "forced_expert must be given iff MOE_F_FORCED_ROUTING");
+  if (!aligned16(x) || !aligned16(wg) || !aligned16(w1) || !aligned16(w2) || !aligned16(y))
+    return fail(MOE_ERR_ALIGN, "tensor pointers must be 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(saved) & 255) return fail(MOE_ERR_ALIGN, "saved must be 256-byte aligned");
+  const Dims& d = c->d;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const SavedLayout& sv = c->sv;
+  const ScratchLayout& sc = c->sc;
+  const SlotSpace ss = slot_space(d);
+  const bool solo = d.world == 1;
+  const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
+
+  // F1 + F2: gate and capacity slots
+  RouteArgs ra;
+  ra.x = x; ra.wg = wg; ra.forced = forced_expert; ra.T = d.T; ra.H = d.H; ra.E = d.E; ra.C = d.C;
+  ra.logits = at<float>(saved, sv.logits);
+  ra.expert = at<int32_t>(saved, sv.expert);
+  ra.prob = at<float>(saved, sv.prob);
+  ra.gap = at<float>(saved, sv.gap);
+  ra.slot = at<int32_t>(saved, sv.slot);
+  ra.count = at<int32_t>(saved, sv.count);
+  ra.load = at<int32_t>(saved, sv.load);
+  ra.tok_of = at<int32_t>(saved, sv.tok_of);
+  ra.local_rank = at<int32_t>(c->scratch, sc.local_rank);
+  ra.block_hist = at<int32_t>(c->scratch, sc.block_hist);
+  ra.ties = at<int32_t>(saved, sv.ties);
+  {
+    Scope sc_(c, MOE_K_ROUTE, st, 3);
+    CUDA_TRY(c, route(ra, st));
+  }
+
+  // F3 dispatch (DTD: only this rank's slot slice), F4 a2a, F5 all-gather
+  void* X = at<uint8_t>(saved, sv.X);
+  void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
+  {
+    Scope sc_(c, MOE_K_DISPATCH, st, 1);
+    CUDA_TRY(c, dispatch(x, ra.tok_of, ra.count, ss, lo, hi, D, st));
+  }
+  if (!solo) {
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(ep_exchange(c, 0, 0, D, X, lo, hi, st));
+    if (d.dtd) TRY(ag_expert(c, 0, X, st));
+  }
+
+  // F6 GEMM1 + GeLU, F7 GEMM2
+  void* Hpre = at<uint8_t>(saved, sv.Hpre);
+  void* A = at<uint8_t>(saved, sv.A);
+  void* O = at<uint8_t>(saved, sv.O);
+  void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
+  GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, Hpre, EPI_GELU, A};
+  TRY(gemm(c, g1, st));
+  GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+  TRY(gemm(c, g2, st));
+
+  // F8 TP reduce, F9 a2a back, F10 all-gather
+  if (!solo) {
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    if (d.Gt > 1) {
+      if (d.dtd) TRY(rs_expert(c, 0, Y, st));
+      else TRY(ar_expert(c, 0, Y, st));
+    }
+    TRY(ep_exchange(c, 1, 0, O, Y, lo, hi, st));
+    if (d.dtd) TRY(ag_slot(c, 0, O, st));
+  }
+
+  // F11 combine
+  {
+    Scope sc_(c, MOE_K_COMBINE, st, 1);
+    CUDA_TRY(c, combine(O, ra.expert, ra.slot, ra.prob, ss, d.T, y, st));
+  }
+  c->saved_written.insert(saved);
+  c->last_saved = saved;
+  c->last_stream = st;
+  return MOE_OK;
+}
+
+moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const void* x,
+                        const float* wg, const void* w1, const void* w2, void* dx, float* dwg,
+                        void* dw1, void* dw2, void* stream) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  if (c->poisoned) return fail(MOE_ERR_STATE, "ctx poisoned by an earlier CUDA/NCCL failure");
+  if (!dy || !saved || !x || !wg || !w1 || !w2 || !dx || !dwg || !dw1 || !dw2)
+    return fail(MOE_ERR_ARG, "null tensor pointer");
+  if (!c->saved_written.count(saved))
+    return fail(MOE_ERR_STATE, "saved blob was not written by moe_forward on this ctx");
+  if (!aligned16(dy) || !aligned16(x) || !aligned16(wg) || !aligned16(w1) || !aligned16(w2) ||
+      !aligned16(dx) || !aligned16(dwg) || !aligned16(dw1) || !aligned16(dw2))
+    return fail(MOE_ERR_ALIGN, "tensor pointers must be 16-byte aligned");
+  const Dims& d = c->d;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const SavedLayout& sv = c->sv;
+  const ScratchLayout& sc = c->sc;
+  const SlotSpace ss = slot_space(d);
+  const bool solo = d.world == 1;
+  const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
+  const int32_t* expert = at<int32_t>(saved, sv.expert);
+  const int32_t* slot = at<int32_t>(saved, sv.slot);
+  const float* prob = at<float>(saved, sv.prob);
+  const float* logits = at<float>(saved, sv.logits);
+  const int32_t* count = at<int32_t>(saved, sv.count);
+  const void* X = at<uint8_t>(saved, sv.X);
+  const void* Hpre = at<uint8_t>(saved, sv.Hpre);
+  const void* A = at<uint8_t>(saved, sv.A);
+  const void* O = at<uint8_t>(saved, sv.O);
+  float* dp = at<float>(c->scratch, sc.dp);
+  void* dY = at<uint8_t>(c->scratch, sc.dY);
+  void* dO = at<uint8_t>(c->scratch, sc.dO);
+  void* dH = at<uint8_t>(c->scratch, sc.dH);
+  void* dXp = at<uint8_t>(c->scratch, sc.dXp);
+  void* dS = at<uint8_t>(c->scratch, sc.dS);
+
+  // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
+  {
+    Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
+    CUDA_TRY(c, combine_bwd(dy, O, expert, slot, prob, count, ss, d.T, lo, hi, dp, dO, st));
+  }
+  if (!solo) {
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(ep_exchange(c, 0, 1, dO, dY, lo, hi, st));
+    if (d.dtd) TRY(ag_expert(c, 1, dY, st));
+  }
+  // B4 dHpre = (dY W2) * gelu'(Hpre); B5 dXpart = dHpre W1; B6 dW2 = dY^T A, dW1 = dHpre^T X
+  GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(Hpre)};
+  TRY(gemm(c, g4, st));
+  GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
+  TRY(gemm(c, g5, st));
+  GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};
+  TRY(gemm(c, g6, st));
+  GemmArgs g7{d.El, d.Fl, d.H, (int)d.R, dH, 1, X, 1, dw1, EPI_STORE, nullptr};
+  TRY(gemm(c, g7, st));
+  // B7 TP reduce, B8 a2a back, B9 all-gather
+  if (!solo) {
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    if (d.Gt > 1) {
+      if (d.dtd) TRY(rs_expert(c, 1, dXp, st));
+      else TRY(ar_expert(c, 1, dXp, st));
+    }
+    TRY(ep_exchange(c, 1, 1, dS, dXp, lo, hi, st));
+    if (d.dtd) TRY(ag_slot(c, 1, dS, st));
+  }
+  // B10 dispatch-bwd + gate-bwd
+  {
+    Scope sc_(c, MOE_K_GATE_BWD, st, 3);
+    CUDA_TRY(c, gate_bwd(x, dS, wg, logits, expert, slot, prob, dp, ss, d.T, dx, dwg,
+                         at<float>(c->scratch, sc.dl), at<float>(c->scratch, sc.dwgp), sc.nsplit, st));
+  }
+  c->last_stream = st;
+  return MOE_OK;
+}
+
+moe_status moe_routing(moe_ctx* c, const void* saved, int32_t* expert, int32_t* slot, float* prob,
+                       float* gap, int32_t* count, void* stream) {
+  if (!c || !saved) return fail(MOE_ERR_ARG, "null ctx/saved");
+  if (!c->saved_written.count(saved)) return fail(MOE_ERR_STATE, "saved blob not written by this ctx");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Dims& d = c->d;
+  const SavedLayout& sv = c->sv;
+  auto cp = [&](void* dst, size_t off, size_t bytes) -> moe_status {
+    if (!dst) return MOE_OK;
+    CUDA_TRY(c, cudaMemcpyAsync(dst, at<uint8_t>(saved, off), bytes, cudaMemcpyDeviceToDevice, st));
+    return MOE_OK;
+  };
+  TRY(cp(expert, sv.expert, (size_t)d.T * 4));
+  TRY(cp(slot, sv.slot, (size_t)d.T * 4));
+  TRY(cp(prob, sv.prob, (size_t)d.T * 4));
+  TRY(cp(gap, sv.gap, (size_t)d.T * 4));
+  TRY(cp(count, sv.count, (size_t)d.E * 4));
+  return MOE_OK;
+}
+
+moe_status moe_stats_get(moe_ctx* c, moe_stats* out) {
+  if (!c || !out) return fail(MOE_ERR_ARG, "null ctx/output");
+  if (c->last_stream) CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
+  if (c->last_saved) {
+    int32_t ties = 0;
+    std::vector<int32_t> count(c->d.E);
+    CUDA_TRY(c, cudaMemcpy(&ties, at<uint8_t>(c->last_saved, c->sv.ties), 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(count.data(), at<uint8_t>(c->last_saved, c->sv.count), 4 * c->d.E,
+                           cudaMemcpyDeviceToHost));
+    int64_t kept = 0;
+    for (int32_t v : count) kept += v;
+    c->stats.tie_tokens = ties;
+    c->stats.dropped_tokens = c->d.T - kept;
+  }
+  for (auto& sp : c->spans) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) c->stats.kernel_ms[sp.cls] += ms;
+    c->pool.push_back(sp.a);
+    c->pool.push_back(sp.b);
+  }
+  c->spans.clear();
+  c->stats.nccl_async_error = 0;
+  ncclComm_t comms[3] = {c->world_comm, c->tp_comm, c->ep_comm};
+  for (ncclComm_t m : comms) {
+    if (!m) continue;
+    ncclResult_t ae = ncclSuccess;
+    if (ncclCommGetAsyncError(m, &ae) == ncclSuccess && ae != ncclSuccess) c->stats.nccl_async_error = (int)ae;
+  }
+  *out = c->stats;
+  return MOE_OK;
+}
+
+moe_status moe_stats_reset(moe_ctx* c) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  std::memset(&c->stats, 0, sizeof(c->stats));
+  return MOE_OK;
+}
+
+moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn, const void* B,
+                         int b_mn, void* D, int epilogue, void* aux, int impl, void* stream) {
+  if (batch < 0 || M < 0 || N < 0 || K < 0) return fail(MOE_ERR_ARG, "negative size");
+  if (!A || !B || !D) return fail(MOE_ERR_ARG, "null operand");
+  if (epilogue < 0 || epilogue > 2) return fail(MOE_ERR_ARG, "bad epilogue");
+  if (epilogue != EPI_STORE && !aux) return fail(MOE_ERR_ARG, "epilogue needs aux");
+  if (N % 64 || M % 8 || K % 8) return fail(MOE_ERR_SHAPE, "need N % 64 == 0, M % 8 == 0, K % 8 == 0");
+  if (!aligned16(A) || !aligned16(B) || !aligned16(D) || (aux && !aligned16(aux)))
+    return fail(MOE_ERR_ALIGN, "operands must be 16-byte aligned");
+  GemmArgs g{batch, M, N, K, A, a_mn ? 1 : 0, B, b_mn ? 1 : 0, D, epilogue, aux};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (impl == 1) {
+    cudaError_t e = gemm_ref(g, st);
+    if (e != cudaSuccess) return fail(MOE_ERR_CUDA, cudaGetErrorString(e));
+    return MOE_OK;
+  }
+  return gemm(nullptr, g, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// internal.h — host-side declarations shared by the libmoe translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace moe {
+
+// Batched GEMM D[b] = epi(A[b] . B[b]^T); layouts as in moe.h (moe_gemm_bf16).
+enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2 };
+
+struct GemmArgs {
+  int batch, M, N, K;
+  const void* A;
+  int a_mn;  // 0: A [b][M][K]; 1: A [b][K][M]
+  const void* B;
+  int b_mn;  // 0: B [b][N][K]; 1: B [b][K][N]
+  void* D;   // [b][M][N]
+  int epilogue;
+  void* aux;  // EPI_GELU: out [b][M][N]; EPI_DGELU: in (Hpre) [b][M][N]
+};
+
+// tcgen05 / TMEM / TMA kernel (the product path).
+cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why);
+// Plain SIMT kernel: bring-up cross-check only (moe_gemm_bf16 impl=1).
+cudaError_t gemm_ref(const GemmArgs& a, cudaStream_t s);
+
+// ---- routing / permutation kernels (route.cu, permute.cu) ----
+struct RouteArgs {
+  const void* x;        // bf16 [T][H]
+  const float* wg;      // [H][E]
+  const int32_t* forced;  // [T] or null
+  int64_t T;
+  int H, E;
+  int64_t C;
+  float* logits;        // [T][E]
+  int32_t* expert;      // [T]
+  float* prob;          // [T]
+  float* gap;           // [T]
+  int32_t* slot;        // [T]
+  int32_t* count;       // [E]   kept per expert
+  int32_t* load;        // [E]   routed per expert (pre-capacity)
+  int32_t* tok_of;      // [E][C] token of (expert, slot), valid for slot < count
+  int32_t* local_rank;  // scratch [T]
+  int32_t* block_hist;  // scratch [ceil(T/1024)][E]
+  int32_t* ties;        // [1]: tokens with gap < 1e-6
+};
+cudaError_t route(const RouteArgs& a, cudaStream_t s);
+
+// Slot-space layout [G_t][E][C_s][H]: slot c of expert e lives at slice c / C_s.
+struct SlotSpace {
+  int64_t C, Cs;  // capacity and slot-slice size
+  int G_t, E, H;
+};
+
+// F3: D[tt][e][cs] = x[tok_of[e][tt*Cs+cs]] (zeros for empty slots), for slices
+// tt in [t_lo, t_hi).
+cudaError_t dispatch(const void* x, const int32_t* tok_of, const int32_t* count,
+                     const SlotSpace& ss, int t_lo, int t_hi, void* D, cudaStream_t s);
+
+// F11: y_t = bf16(p_t * O[row(t)]), 0 if dropped.
+cudaError_t combine(const void* O, const int32_t* expert, const int32_t* slot, const float* prob,
+                    const SlotSpace& ss, int64_t T, void* y, cudaStream_t s);
+
+// B1: dp_t = <dy_t, O[row(t)]> (fp32), dO[row(t)] = bf16(p_t dy_t) for kept
+// tokens whose slot lies in slices [t_lo, t_hi); empty slots in those slices -> 0.
+cudaError_t combine_bwd(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
+                        const float* prob, const int32_t* count, const SlotSpace& ss, int64_t T,
+                        int t_lo, int t_hi, float* dp, void* dO, cudaStream_t s);
+
+// B10: dx_t = dS[row(t)] + sum_j dl_tj Wg[:, j] (kept), 0 (dropped);
+// dl_tj = dp_t p_t (delta_{j,e*} - softmax(l_t)_j); dWg = sum_t x_t^T dl_t.
+cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float* logits,
+                     const int32_t* expert, const int32_t* slot, const float* prob,
+                     const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
+                     float* dl_scratch, float* dwg_partial, int nsplit, cudaStream_t s);
+int gate_bwd_splits(int64_t T);
+
+}  // namespace moe

@@ -1,0 +1,144 @@
+// plan.cpp — host-only planning: validation (moe.h constraints), the HBM
+// layout of the saved/scratch blobs and the collective schedule/ledger.
+#include "plan.h"
+
+#include <cmath>
+
+#include "internal.h"
+
+namespace moe {
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::string* why) {
+  if (!c || !d) { *why = "null config/output"; return MOE_ERR_ARG; }
+  if (world < 1 || rank < 0 || rank >= world) { *why = "rank/world out of range"; return MOE_ERR_ARG; }
+  if (c->tokens < 1 || c->hidden < 1 || c->ffn < 1 || c->experts < 1 || c->g_tensor < 1 ||
+      c->g_expert < 1 || !(c->capacity_factor > 0.f) || !std::isfinite(c->capacity_factor)) {
+    *why = "tokens, hidden, ffn, experts, g_tensor, g_expert and capacity_factor must be positive";
+    return MOE_ERR_ARG;
+  }
+  if (c->experts > 64) { *why = "experts must be <= 64"; return MOE_ERR_SHAPE; }
+  if (c->hidden % 64) { *why = "hidden % 64 != 0"; return MOE_ERR_SHAPE; }
+  if (c->ffn % c->g_tensor) { *why = "ffn % g_tensor != 0"; return MOE_ERR_SHAPE; }
+  if ((c->ffn / c->g_tensor) % 64) { *why = "(ffn / g_tensor) % 64 != 0"; return MOE_ERR_SHAPE; }
+  if (c->experts % c->g_expert) { *why = "experts % g_expert != 0"; return MOE_ERR_SHAPE; }
+  const int tp_ep = c->g_tensor * c->g_expert;
+  if (world % tp_ep) { *why = "world % (g_tensor * g_expert) != 0"; return MOE_ERR_SHAPE; }
+  if (c->tokens > (int64_t)1 << 30) { *why = "tokens must be < 2^30"; return MOE_ERR_SHAPE; }
+  if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING)) { *why = "unknown flag bits"; return MOE_ERR_ARG; }
+  d->T = c->tokens;
+  d->H = c->hidden;
+  d->F = c->ffn;
+  d->E = c->experts;
+  d->Gt = c->g_tensor;
+  d->Gep = c->g_expert;
+  d->Gd = world / tp_ep;
+  d->world = world;
+  d->rank = rank;
+  d->t = rank % d->Gt;
+  d->ep = (rank / d->Gt) % d->Gep;
+  d->d = rank / tp_ep;
+  d->El = d->E / d->Gep;
+  d->Fl = d->F / d->Gt;
+  // Reading R2: C = ceil(cf*T/E) (double), >= 1, rounded up to a multiple of G_t.
+  int64_t C = (int64_t)std::ceil((double)c->capacity_factor * (double)d->T / (double)d->E);
+  if (C < 1) C = 1;
+  C = ceil_div(C, d->Gt) * d->Gt;
+  d->C = C;
+  d->Cs = C / d->Gt;
+  d->R = (int64_t)d->Gep * C;
+  d->S = world / d->Gt;
+  d->dtd = c->dtd != 0 && d->Gt > 1;
+  d->forced = (c->flags & MOE_F_FORCED_ROUTING) != 0;
+  if (d->R > (int64_t)1 << 30) { *why = "rows per expert too large"; return MOE_ERR_SHAPE; }
+  return MOE_OK;
+}
+
+namespace {
+struct Bump {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  }
+};
+}  // namespace
+
+void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
+  const size_t slot_space = (size_t)d.E * d.C * d.H * 2;            // [G_t][E][C_s][H]
+  const size_t expert_space = (size_t)d.El * d.R * d.H * 2;         // [E_l][R][H]
+  const size_t ffn_space = (size_t)d.El * d.R * d.Fl * 2;           // [E_l][R][F_l]
+  Bump s;
+  sv->logits = s.take((size_t)d.T * d.E * 4);
+  sv->expert = s.take((size_t)d.T * 4);
+  sv->slot = s.take((size_t)d.T * 4);
+  sv->prob = s.take((size_t)d.T * 4);
+  sv->gap = s.take((size_t)d.T * 4);
+  sv->count = s.take((size_t)d.E * 4);
+  sv->load = s.take((size_t)d.E * 4);
+  sv->ties = s.take(4);
+  sv->tok_of = s.take((size_t)d.E * d.C * 4);
+  sv->X = s.take(expert_space);
+  sv->Hpre = s.take(ffn_space);
+  sv->A = s.take(ffn_space);
+  sv->O = s.take(slot_space);
+  sv->total = s.off;
+
+  const bool solo = d.world == 1;  // slot space == expert space, no communication
+  sc->D_in_saved = solo;
+  sc->Y_in_saved = solo;
+  sc->dO_is_dY = solo;
+  sc->dXp_is_dS = solo;
+  sc->nsplit = gate_bwd_splits(d.T);
+  Bump f;
+  sc->local_rank = f.take((size_t)d.T * 4);
+  sc->block_hist = f.take((size_t)((d.T + 1023) / 1024) * d.E * 4);
+  sc->D = solo ? 0 : f.take(slot_space);
+  sc->Ypart = solo ? 0 : f.take(expert_space);
+  Bump b;  // backward region reuses the forward region
+  sc->dp = b.take((size_t)d.T * 4);
+  sc->dl = b.take((size_t)d.T * d.E * 4);
+  sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
+  sc->dY = b.take(expert_space);
+  sc->dO = solo ? sc->dY : b.take(slot_space);
+  sc->dH = b.take(ffn_space);
+  sc->dXp = b.take(expert_space);
+  sc->dS = solo ? sc->dXp : b.take(slot_space);
+  sc->total = f.off > b.off ? f.off : b.off;
+}
+
+std::vector<moe_collective> make_schedule(const Dims& d) {
+  std::vector<moe_collective> v;
+  const int64_t elt = 2;  // bf16
+  const int64_t slices = d.dtd ? 1 : d.Gt;  // slot slices a rank sends per expert
+  auto push = [&](int kind, int pass, int step, int gsize, int64_t buf, int64_t wire) {
+    moe_collective c;
+    c.kind = kind; c.pass = pass; c.step = step; c.group_size = gsize;
+    c.buffer_bytes = buf; c.wire_bytes = wire;
+    v.push_back(c);
+  };
+  const int64_t a2a_buf = (int64_t)d.E * slices * d.Cs * d.H * elt;       // send buffer incl. self
+  const int64_t a2a_wire = (int64_t)(d.Gep - 1) * d.El * slices * d.Cs * d.H * elt;
+  const int64_t xe = (int64_t)d.El * d.R * d.H * elt;                       // expert-space buffer
+  const int64_t O = (int64_t)d.E * d.C * d.H * elt;                         // slot-space buffer
+  const int64_t g = d.Gt;
+  for (int pass = 0; pass < 2; ++pass) {
+    // forward: F4 a2a, F5 AG (DTD), [GEMMs], F8 RS/AR, F9 a2a, F10 AG (DTD)
+    // backward mirrors it: B2 a2a, B3 AG (DTD), [GEMMs], B7 RS/AR, B8 a2a, B9 AG (DTD)
+    const int s_a2a1 = pass ? 2 : 4, s_ag1 = pass ? 3 : 5, s_red = pass ? 7 : 8;
+    const int s_a2a2 = pass ? 8 : 9, s_ag2 = pass ? 9 : 10;
+    if (d.Gep > 1) push(MOE_COLL_A2A, pass, s_a2a1, d.Gep, a2a_buf, a2a_wire);
+    if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag1, d.Gt, xe, xe * (g - 1) / g);
+    if (d.Gt > 1) {
+      if (d.dtd) push(MOE_COLL_REDUCESCATTER, pass, s_red, d.Gt, xe, xe * (g - 1) / g);
+      else push(MOE_COLL_ALLREDUCE, pass, s_red, d.Gt, xe, 2 * xe * (g - 1) / g);
+    }
+    if (d.Gep > 1) push(MOE_COLL_A2A, pass, s_a2a2, d.Gep, a2a_buf, a2a_wire);
+    if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag2, d.Gt, O, O * (g - 1) / g);
+  }
+  return v;
+}
+
+}  // namespace moe

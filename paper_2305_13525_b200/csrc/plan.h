@@ -1,0 +1,49 @@
+// plan.h — derived dimensions, buffer layouts and the collective schedule.
+// Pure host code (no CUDA calls) so the CPU tests can check it without a GPU.
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/moe.h"
+
+namespace moe {
+
+struct Dims {
+  int64_t T;
+  int H, F, E;
+  int Gt, Gep, Gd, world, rank;
+  int d, ep, t;
+  int El, Fl;
+  int64_t C, Cs, R;  // capacity, slot slice, rows per local expert
+  int S;             // token groups
+  bool dtd;          // DTD in effect (requested and G_t > 1)
+  bool forced;
+};
+
+// Validates and derives; returns MOE_OK or an error with *why set.
+moe_status make_dims(const moe_config* cfg, int world, int rank, Dims* d, std::string* why);
+
+struct SavedLayout {
+  size_t logits, expert, slot, prob, gap, count, load, ties, tok_of, X, Hpre, A, O, total;
+};
+struct ScratchLayout {
+  // forward
+  size_t local_rank, block_hist, D, Ypart;
+  // backward
+  size_t dp, dl, dwgp, dO, dY, dH, dXp, dS;
+  size_t total;
+  bool D_in_saved, Y_in_saved;  // world == 1: D aliases saved.X, Ypart aliases saved.O
+  bool dO_is_dY, dXp_is_dS;     // world == 1: slot space == expert space
+  int nsplit;
+};
+
+void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc);
+
+// Collective schedule of one forward + backward on this rank (issue order).
+std::vector<moe_collective> make_schedule(const Dims& d);
+
+}  // namespace moe

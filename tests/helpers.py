@@ -1,0 +1,55 @@
+"""Shared test helpers: seeded inputs -> torch/oracle, parity metrics, tie protocol."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import moe_oracle as O
+from paper_2305_13525_b200 import synth
+
+REL_L2_BAR = 1e-2  # BASELINE.json north_star: relative L2 <= 1e-2 (bf16, fp32 accumulate)
+
+
+def bf16_tensor(bits: np.ndarray, device="cuda") -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(device)
+
+
+def tensor_f64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def rel_l2(got, ref) -> float:
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    nr = np.linalg.norm(ref)
+    if nr == 0:
+        return 0.0 if np.linalg.norm(got) == 0 else np.inf
+    return float(np.linalg.norm(got - ref) / nr)
+
+
+class Inputs:
+    """Seeded inputs of one workload (all token groups), as bf16 bits + fp32 Wg."""
+
+    def __init__(self, shape: synth.LayerShape, tokens: int | None = None, skew: float = 1.0):
+        self.shape = shape
+        self.T = shape.tokens if tokens is None else tokens
+        S = shape.groups
+        self.x = [synth.make_x(shape, s, self.T) for s in range(S)]
+        self.dy = [synth.make_dy(shape, s, self.T) for s in range(S)]
+        self.wg = synth.make_wg(shape, skew)
+        self.w1, self.w2 = synth.make_experts(shape)
+
+    def oracle_arrays(self):
+        return ([O.decode_bf16(a) for a in self.x], [O.decode_bf16(a) for a in self.dy],
+                self.wg.astype(np.float64), O.decode_bf16(self.w1), O.decode_bf16(self.w2))
+
+
+def routing_protocol(gpu_expert, gpu_gap, r: O.Routing):
+    """SURVEY §8(c) comparison step 2: argmax must match outside the tie set
+    (top-2 gap < 1e-6 on either side); returns (tie_idx, override experts)."""
+    ge = np.asarray(gpu_expert)
+    tie = (r.gap < O.TIE_GAP) | (np.asarray(gpu_gap) < O.TIE_GAP)
+    bad = np.nonzero((ge != r.expert) & ~tie)[0]
+    assert bad.size == 0, f"routing mismatch outside tie set at tokens {bad[:10]}"
+    idx = np.nonzero(tie)[0]
+    return idx, ge[idx]

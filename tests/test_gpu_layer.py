@@ -1,0 +1,185 @@
+"""MoE layer (1 GPU, G = 1) through the C ABI vs the CPU oracle.
+
+Routing: bit-exact outside logged ties (BASELINE.json); slots/count/dropped
+sets bit-exact after the tie-override protocol.
+Floating outputs: relative L2 <= 1e-2 for y, dx, dWg, dW1, dW2.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+from paper_2305_13525_b200 import MoEConfig, MoELayer, synth
+from tests.helpers import REL_L2_BAR, Inputs, bf16_tensor, rel_l2, routing_protocol, tensor_f64
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(inp: Inputs, shape, forced=None, cf=None):
+    cfg = MoEConfig(inp.T, shape.hidden, shape.ffn, shape.experts,
+                    shape.cf if cf is None else cf, 1, 1, True, 1 | (2 if forced is not None else 0))
+    layer = MoELayer(cfg)
+    x = bf16_tensor(inp.x[0])
+    dy = bf16_tensor(inp.dy[0])
+    wg = torch.from_numpy(inp.wg).cuda()
+    w1 = bf16_tensor(inp.w1)
+    w2 = bf16_tensor(inp.w2)
+    f = None if forced is None else torch.from_numpy(forced).cuda()
+    y, saved = layer.moe_forward(x, wg, w1, w2, forced=f)
+    dx, dwg, dw1, dw2 = layer.moe_backward(dy, saved, x, wg, w1, w2)
+    rt = layer.moe_routing(saved)
+    torch.cuda.synchronize()
+    out = {"y": tensor_f64(y), "dx": tensor_f64(dx), "dwg": dwg.cpu().numpy().astype(np.float64),
+           "dw1": tensor_f64(dw1), "dw2": tensor_f64(dw2),
+           **{k: v.cpu().numpy() for k, v in rt.items()}, "stats": layer.moe_stats()}
+    layer.close()
+    return out, cfg
+
+
+def check_parity(inp: Inputs, g, cf, forced=None):
+    xs, dys, wg, w1, w2 = inp.oracle_arrays()
+    cap = O.capacity(inp.T, wg.shape[1], cf, 1)
+    r0 = O.route(xs[0], wg, cap, forced=forced)
+    if forced is None:
+        idx, ex = routing_protocol(g["expert"], g["gap"], r0)
+        override = [(idx, ex)]
+    else:
+        np.testing.assert_array_equal(g["expert"], forced)
+        override = None
+    ref = O.layer(xs, dys, wg, w1, w2, cf, 1, forced=None if forced is None else [forced],
+                  overrides=override)
+    r = ref["routing"][0]
+    np.testing.assert_array_equal(g["slot"], r.slot)
+    np.testing.assert_array_equal(g["count"], r.count)
+    np.testing.assert_allclose(g["prob"], r.p, rtol=1e-5, atol=1e-7)
+    assert g["stats"]["dropped_tokens"] == int((~r.kept).sum())
+    errs = {"y": rel_l2(g["y"], ref["y"][0]), "dx": rel_l2(g["dx"], ref["dx"][0]),
+            "dwg": rel_l2(g["dwg"], ref["dwg"][0]), "dw1": rel_l2(g["dw1"], ref["dw1"]),
+            "dw2": rel_l2(g["dw2"], ref["dw2"])}
+    for k, v in errs.items():
+        assert v <= REL_L2_BAR, (k, errs)
+    # dropped tokens are exact zeros
+    assert (g["y"][~r.kept] == 0).all() and (g["dx"][~r.kept] == 0).all()
+    return errs
+
+
+@pytest.mark.parametrize("cf", [1.0, 0.5, 2.0])
+def test_tiny_layer_parity(cf):
+    shape = synth.CONFIGS["tiny"]
+    inp = Inputs(shape)
+    g, _ = run_gpu(inp, shape, cf=cf)
+    check_parity(inp, g, cf)
+
+
+def test_tiny_skewed_drops():
+    shape = synth.CONFIGS["tiny"]
+    inp = Inputs(shape, skew=1.5)
+    g, _ = run_gpu(inp, shape)
+    errs = check_parity(inp, g, 1.0)
+    assert g["stats"]["dropped_tokens"] > 0, errs
+
+
+@pytest.mark.parametrize("mode", ["round_robin", "all_to_one", "random"])
+def test_tiny_forced_routing(mode):
+    shape = synth.CONFIGS["tiny"]
+    inp = Inputs(shape)
+    forced = synth.forced_routing(mode, inp.T, shape.experts)
+    g, _ = run_gpu(inp, shape, forced=forced)
+    check_parity(inp, g, 1.0, forced=forced)
+    if mode == "round_robin":
+        assert g["stats"]["dropped_tokens"] == 0
+    if mode == "all_to_one":
+        assert g["count"][0] == g["count"].sum() == O.capacity(inp.T, shape.experts, 1.0)
+
+
+@pytest.mark.parametrize("T,H,F,E", [(1000, 128, 192, 5), (2048, 256, 512, 16), (3000, 320, 640, 32),
+                                     (777, 64, 128, 64), (1, 64, 64, 3)])
+def test_ragged_shapes(T, H, F, E):
+    shape = synth.LayerShape("ragged", T, H, F, E)
+    inp = Inputs(shape)
+    g, _ = run_gpu(inp, shape)
+    check_parity(inp, g, 1.0)
+
+
+def test_exact_tie_lowest_index():
+    shape = synth.LayerShape("tie", 512, 128, 256, 8)
+    inp = Inputs(shape)
+    inp.wg[:, 5] = inp.wg[:, 2]  # exact ties between experts 2 and 5
+    g, _ = run_gpu(inp, shape)
+    xs, dys, wg, w1, w2 = inp.oracle_arrays()
+    r = O.route(xs[0], wg, O.capacity(512, 8, 1.0))
+    tied = r.expert == 2
+    assert (g["expert"][tied] == 2).all() and not (g["expert"] == 5).any()
+    assert g["stats"]["tie_tokens"] >= int(tied.sum())
+    check_parity(inp, g, 1.0)
+
+
+def test_13b_reduced_tokens_full_parity():
+    """1.3B shapes (H 2048, F 8192, E 16) at T = 2048, every output element."""
+    shape = synth.CONFIGS["1.3b"]
+    inp = Inputs(shape, tokens=2048)
+    g, _ = run_gpu(inp, shape)
+    check_parity(inp, g, 1.0)
+
+
+def test_13b_full_size_sampled():
+    """BASELINE configs[1] at full size (T = 16384) in the bench's launch
+    configuration: routing bit-exact for all tokens; y/dx on sampled tokens;
+    dW1 rows / dW2 columns on sampled (expert, f)."""
+    shape = synth.CONFIGS["1.3b"]
+    inp = Inputs(shape)
+    g, _ = run_gpu(inp, shape)
+    xs, dys, wg, w1, w2 = inp.oracle_arrays()
+    cap = O.capacity(inp.T, shape.experts, 1.0)
+    r0 = O.route(xs[0], wg, cap)
+    idx, ex = routing_protocol(g["expert"], g["gap"], r0)
+    r = O.route(xs[0], wg, cap, override=(idx, ex))
+    np.testing.assert_array_equal(g["slot"], r.slot)
+    np.testing.assert_array_equal(g["count"], r.count)
+    rng = np.random.default_rng(0)
+    toks = np.concatenate([rng.choice(inp.T, 48, replace=False), np.nonzero(~r.kept)[0][:4], [0, inp.T - 1]])
+    ys, yr, dxs, dxr = [], [], [], []
+    for t in toks:
+        yt, _ = O.token_forward(int(t), xs[0], w1, w2, r)
+        ys.append(g["y"][t]); yr.append(yt)
+        dxs.append(g["dx"][t]); dxr.append(O.token_backward(int(t), xs[0], dys[0], wg, w1, w2, r))
+    assert rel_l2(ys, yr) <= REL_L2_BAR
+    assert rel_l2(dxs, dxr) <= REL_L2_BAR
+    g1s, g1r, g2s, g2r = [], [], [], []
+    for e, f in [(0, 0), (3, 8191), (7, 1234), (15, 4096), (11, 77)]:
+        a, b = O.expert_row_grads(e, f, xs, dys, w1, w2, [r])
+        g1s.append(g["dw1"][e, f]); g1r.append(a)
+        g2s.append(g["dw2"][e, :, f]); g2r.append(b)
+    assert rel_l2(g1s, g1r) <= REL_L2_BAR
+    assert rel_l2(g2s, g2r) <= REL_L2_BAR
+
+
+def test_determinism_bitwise():
+    shape = synth.LayerShape("det", 4096, 256, 512, 16)
+    inp = Inputs(shape)
+    a, _ = run_gpu(inp, shape)
+    b, _ = run_gpu(inp, shape)
+    for k in ("y", "dx", "dwg", "dw1", "dw2", "slot"):
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_forward_errors_are_status_codes():
+    from paper_2305_13525_b200 import MoEError
+    shape = synth.CONFIGS["tiny"]
+    layer = MoELayer(MoEConfig.from_shape(shape))
+    x = torch.zeros(shape.tokens, shape.hidden, dtype=torch.bfloat16, device="cuda")
+    wg = torch.zeros(shape.hidden, shape.experts, device="cuda")
+    w1 = torch.zeros(shape.experts, shape.ffn, shape.hidden, dtype=torch.bfloat16, device="cuda")
+    w2 = torch.zeros(shape.experts, shape.hidden, shape.ffn, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(MoEError) as ei:  # forced routing not enabled
+        layer.moe_forward(x, wg, w1, w2, forced=torch.zeros(shape.tokens, dtype=torch.int32, device="cuda"))
+    assert ei.value.name == "MOE_ERR_ARG"
+    bogus = layer.new_saved()
+    with pytest.raises(MoEError) as ei:  # saved blob never written by moe_forward
+        layer.moe_backward(x, bogus, x, wg, w1, w2)
+    assert ei.value.name == "MOE_ERR_STATE"
+    # x = 0: every token routes to expert 0 with p = 1/E (oracle special case)
+    y, saved = layer.moe_forward(x, wg, w1, w2)
+    rt = layer.moe_routing(saved)
+    assert (rt["expert"] == 0).all() and torch.allclose(rt["prob"], torch.full_like(rt["prob"], 0.25))
+    layer.close()
