@@ -159,3 +159,58 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 }  // namespace moe
+
+namespace moe {
+
+// ---------------------------------------------------------------- packed fp32 (sm_100)
+// d.xy += a.xy * b.xy in one fma.rn.f32x2 (two IEEE fp32 FMAs).
+__device__ __forceinline__ void ffma2(float2& d, const float2 a, const float2 b) {
+  unsigned long long& dd = *reinterpret_cast<unsigned long long*>(&d);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;"
+      : "+l"(dd)
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+}
+
+// ---------------------------------------------------------------- gate weight staging
+// Wg [H][E] fp32 is staged in shared memory per H-chunk of `hch` (multiple of 64)
+// as ws[e][blk][half][l8][4] with h_local = 64 blk + 8 l8 + 4 half + q, so the
+// 8 lanes of a token group read one contiguous 128 B line per LDS.128 and the
+// four token groups of the warp share it by broadcast.
+__device__ __forceinline__ int ws_index(int e, int hl, int hch) {
+  const int blk = hl >> 6, r = hl & 63, l8 = r >> 3, half = (r >> 2) & 1, q = r & 3;
+  return e * hch + blk * 64 + half * 32 + l8 * 4 + q;
+}
+
+// Coalesced over the global [H][E] array; entries for h >= H are zero. 16 loads
+// per thread are issued before their shared-memory stores (one dependent L2
+// round trip per 16 elements instead of per element).
+__device__ __forceinline__ void stage_wg(float* ws, const float* __restrict__ wg, int h0, int hch,
+                                         int H, int E) {
+  constexpr int U = 16;
+  const int n = hch * E;
+  const int nt = blockDim.x;
+  const float* src = wg + (size_t)h0 * E;
+  const int valid = (H - h0 < hch ? H - h0 : hch) * E;
+  for (int b = threadIdx.x; b < n; b += U * nt) {
+    float v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = b + k * nt;
+      v[k] = i < valid ? __ldg(src + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = b + k * nt;
+      if (i < n) {
+        const int hl = i / E, e = i - hl * E;
+        ws[ws_index(e, hl, hch)] = v[k];
+      }
+    }
+  }
+}
+
+// Largest multiple of 64 with hch * emax * 4 <= 128 KiB.
+__host__ __device__ constexpr int wg_chunk(int emax) { return (128 * 1024 / (emax * 4)) & ~63; }
+
+}  // namespace moe

@@ -14,6 +14,7 @@ namespace moe {
 namespace {
 
 constexpr int WARPS = 8;
+constexpr int PD = 4;  // prefetch depth (64-wide H steps) of the gate-backward pipeline
 
 __device__ __forceinline__ size_t slot_row(const SlotSpace& ss, int e, int64_t c) {
   const int64_t tt = c / ss.Cs, cs = c - tt * ss.Cs;
@@ -171,174 +172,227 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 // ---------------------------------------------------------------- B10 gate backward
-constexpr int HC = 256;
-
 // dx_t = dS[row(t)] + sum_j dl_tj Wg[h, j]; dl_tj = dp_t p_t (delta_{j e*} - s_tj).
-template <int EMAX, int TPW>
-__global__ void __launch_bounds__(WARPS * 32)
+// Same lane layout and Wg staging as the forward gate (route.cu): 4 token groups
+// of 8 lanes per warp, TPW tokens per lane, packed fma.rn.f32x2 over h pairs.
+template <int EMAX, int TPW, int GW>
+__global__ void __launch_bounds__(GW * 32, 1)
     gate_bwd_dx_kernel(const bf16* __restrict__ dS, const float* __restrict__ wg,
                        const float* __restrict__ logits, const int32_t* __restrict__ expert,
                        const int32_t* __restrict__ slot, const float* __restrict__ prob,
-                       const float* __restrict__ dp, SlotSpace ss, int64_t T,
+                       const float* __restrict__ dp, SlotSpace ss, int64_t T, int hch,
                        bf16* __restrict__ dx, float* __restrict__ dl_out) {
-  extern __shared__ __align__(16) float ws[];  // [EMAX * HC]
+  extern __shared__ __align__(16) float ws[];  // [EMAX][hch], see ws_index
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tok0 = ((int64_t)blockIdx.x * WARPS + warp) * TPW;
+  const int q = lane >> 3, l8 = lane & 7;
   const int E = ss.E, H = ss.H;
-  float dl[TPW][EMAX];
-  size_t row[TPW];
-  bool kept[TPW];
+  constexpr int PER_WARP = 4 * TPW;
+  constexpr int PER_CTA = GW * PER_WARP;
+  const int nchunks = (H + hch - 1) / hch;
+  const bool resident = nchunks == 1;
+  if (resident) {
+    stage_wg(ws, wg, 0, hch, H, E);
+    __syncthreads();
+  }
+  const int64_t nbatch = (T + PER_CTA - 1) / PER_CTA;
+  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+    const int64_t base = b * PER_CTA + warp * PER_WARP + q;
+    float2 dl2[TPW][EMAX];  // (dl, dl) pairs
+    size_t row[TPW];
+    bool kept[TPW], valid[TPW];
 #pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int64_t tok = tok0 + t;
-    kept[t] = false;
-    row[t] = 0;
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t tok = base + 4 * i;
+      valid[i] = tok < T;
+      kept[i] = valid[i] && slot[tok] >= 0;
+      row[i] = 0;
+      float d[EMAX];
 #pragma unroll
-    for (int j = 0; j < EMAX; ++j) dl[t][j] = 0.f;
-    if (tok < T && slot[tok] >= 0) {
-      kept[t] = true;
-      const int e = expert[tok];
-      row[t] = slot_row(ss, e, slot[tok]);
-      float m = -3.402823e38f;
-#pragma unroll
-      for (int j = 0; j < EMAX; ++j)
-        if (j < E) m = fmaxf(m, logits[(size_t)tok * E + j]);
-      float den = 0.f;
-#pragma unroll
-      for (int j = 0; j < EMAX; ++j)
-        if (j < E) {
-          dl[t][j] = expf(logits[(size_t)tok * E + j] - m);
-          den += dl[t][j];
-        }
-      const float g = dp[tok] * prob[tok];
-      const float inv = 1.0f / den;
-#pragma unroll
-      for (int j = 0; j < EMAX; ++j) dl[t][j] = g * ((j == e ? 1.f : 0.f) - dl[t][j] * inv);
-    }
-    if (tok < T && lane < EMAX && lane < E) {
-      float v = 0.f;
-#pragma unroll
-      for (int j = 0; j < EMAX; ++j)
-        if (j == lane) v = dl[t][j];
-      dl_out[(size_t)tok * E + lane] = v;
-      if (EMAX > 32 && lane + 32 < E) {
-        float v2 = 0.f;
+      for (int j = 0; j < EMAX; ++j) d[j] = 0.f;
+      if (kept[i]) {
+        const int e = expert[tok];
+        row[i] = slot_row(ss, e, slot[tok]);
+        float m = -3.402823e38f;
 #pragma unroll
         for (int j = 0; j < EMAX; ++j)
-          if (j == lane + 32) v2 = dl[t][j];
-        dl_out[(size_t)tok * E + lane + 32] = v2;
-      }
-    }
-  }
-  for (int h0 = 0; h0 < H; h0 += HC) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < EMAX * HC; i += blockDim.x) {
-      const int j = i / HC, hl = i % HC;
-      const int l = hl >> 3, half = (hl >> 2) & 1, q = hl & 3;
-      const int h = h0 + hl;
-      ws[j * HC + half * 128 + l * 4 + q] = (j < E && h < H) ? wg[(size_t)h * E + j] : 0.f;
-    }
-    __syncthreads();
-    const int h = h0 + 8 * lane;
-    if (h >= H) continue;
+          if (j < E) m = fmaxf(m, logits[(size_t)tok * E + j]);
+        float den = 0.f;
 #pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      const int64_t tok = tok0 + t;
-      if (tok >= T) continue;
-      bf16* dst = dx + (size_t)tok * H + h;
-      if (!kept[t]) {
-        st_v4(dst, make_uint4(0, 0, 0, 0));
-        continue;
-      }
-      const uint4 u = ld_nc_v4(dS + row[t] + h);
-      float o[8];
-      float2 f0 = unpack_bf16x2(u.x), f1 = unpack_bf16x2(u.y), f2 = unpack_bf16x2(u.z),
-             f3 = unpack_bf16x2(u.w);
-      o[0] = f0.x; o[1] = f0.y; o[2] = f1.x; o[3] = f1.y;
-      o[4] = f2.x; o[5] = f2.y; o[6] = f3.x; o[7] = f3.y;
-      float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < EMAX; ++j)
+          if (j < E) {
+            d[j] = expf(logits[(size_t)tok * E + j] - m);
+            den += d[j];
+          }
+        const float g = dp[tok] * prob[tok];
+        const float inv = 1.0f / den;
 #pragma unroll
-      for (int j = 0; j < EMAX; ++j) {
-        const float4 w0 = *reinterpret_cast<const float4*>(&ws[j * HC + lane * 4]);
-        const float4 w1 = *reinterpret_cast<const float4*>(&ws[j * HC + 128 + lane * 4]);
-        const float d = dl[t][j];
-        g[0] = fmaf(d, w0.x, g[0]); g[1] = fmaf(d, w0.y, g[1]);
-        g[2] = fmaf(d, w0.z, g[2]); g[3] = fmaf(d, w0.w, g[3]);
-        g[4] = fmaf(d, w1.x, g[4]); g[5] = fmaf(d, w1.y, g[5]);
-        g[6] = fmaf(d, w1.z, g[6]); g[7] = fmaf(d, w1.w, g[7]);
+        for (int j = 0; j < EMAX; ++j) d[j] = j < E ? g * ((j == e ? 1.f : 0.f) - d[j] * inv) : 0.f;
       }
-      st_v4(dst, make_uint4(pack_bf16x2(o[0] + g[0], o[1] + g[1]), pack_bf16x2(o[2] + g[2], o[3] + g[3]),
-                            pack_bf16x2(o[4] + g[4], o[5] + g[5]), pack_bf16x2(o[6] + g[6], o[7] + g[7])));
+      if (valid[i] && l8 == 0) {
+#pragma unroll
+        for (int j = 0; j < EMAX; ++j)
+          if (j < E) dl_out[(size_t)tok * E + j] = d[j];
+      }
+#pragma unroll
+      for (int j = 0; j < EMAX; ++j) dl2[i][j] = make_float2(d[j], d[j]);
+    }
+    for (int c = 0; c < nchunks; ++c) {
+      const int h0 = c * hch;
+      if (!resident) {
+        __syncthreads();
+        stage_wg(ws, wg, h0, hch, H, E);
+        __syncthreads();
+      }
+      const int nblk = (H - h0 < hch ? H - h0 : hch) >> 6;
+      // software pipeline: dS for steps blk .. blk+PD-1 in flight
+      uint4 buf[PD][TPW];
+#pragma unroll
+      for (int s = 0; s < PD; ++s)
+#pragma unroll
+        for (int i = 0; i < TPW; ++i)
+          buf[s][i] = (kept[i] && s < nblk) ? ld_nc_v4(dS + row[i] + h0 + 64 * s + 8 * l8)
+                                            : make_uint4(0, 0, 0, 0);
+      for (int blk0 = 0; blk0 < nblk; blk0 += PD) {
+#pragma unroll
+        for (int s = 0; s < PD; ++s) {
+          const int blk = blk0 + s;
+          if (blk < nblk) {
+            const int h = h0 + 64 * blk + 8 * l8;
+            float2 o[TPW][4];
+#pragma unroll
+            for (int i = 0; i < TPW; ++i) {
+              o[i][0] = unpack_bf16x2(buf[s][i].x); o[i][1] = unpack_bf16x2(buf[s][i].y);
+              o[i][2] = unpack_bf16x2(buf[s][i].z); o[i][3] = unpack_bf16x2(buf[s][i].w);
+              if (kept[i] && blk + PD < nblk) buf[s][i] = ld_nc_v4(dS + row[i] + h + 64 * PD);
+            }
+            const float* wrow = ws + blk * 64 + l8 * 4;
+#pragma unroll
+            for (int j = 0; j < EMAX; ++j) {
+              const float4 w0 = *reinterpret_cast<const float4*>(wrow + j * hch);
+              const float4 w1 = *reinterpret_cast<const float4*>(wrow + j * hch + 32);
+              const float2 p0 = make_float2(w0.x, w0.y), p1 = make_float2(w0.z, w0.w);
+              const float2 p2 = make_float2(w1.x, w1.y), p3 = make_float2(w1.z, w1.w);
+#pragma unroll
+              for (int i = 0; i < TPW; ++i) {
+                ffma2(o[i][0], dl2[i][j], p0);
+                ffma2(o[i][1], dl2[i][j], p1);
+                ffma2(o[i][2], dl2[i][j], p2);
+                ffma2(o[i][3], dl2[i][j], p3);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < TPW; ++i) {
+              if (!valid[i]) continue;
+              const uint4 v = kept[i] ? make_uint4(pack_bf16x2(o[i][0].x, o[i][0].y),
+                                                   pack_bf16x2(o[i][1].x, o[i][1].y),
+                                                   pack_bf16x2(o[i][2].x, o[i][2].y),
+                                                   pack_bf16x2(o[i][3].x, o[i][3].y))
+                                      : make_uint4(0, 0, 0, 0);
+              st_v4(dx + (size_t)(base + 4 * i) * H + h, v);
+            }
+          }
+        }
+      }
     }
   }
 }
 
-// dWg partials: CTA (h block of 256, token split s) -> partial[s][h][j].
-// Thread (hq, jg): 4 consecutive h x EMAX/4 experts.
-constexpr int DWG_TT = 32;
+// dWg = x^T dl: CTA (h block of HB, token split) -> partial[split][h][j]. Thread
+// tile 8 h x JT j; x tile staged as fp32 [TT][half][hq][4] (conflict-free LDS.128),
+// dl staged as (dl, dl) pairs so fma.rn.f32x2 runs over h pairs.
+constexpr int DWG_TT = 16;
 template <int EMAX>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
     dwg_partial_kernel(const bf16* __restrict__ x, const float* __restrict__ dl, int64_t T, int H,
                        int E, int64_t tok_per_split, float* __restrict__ partial) {
-  constexpr int EJ = EMAX / 4;
-  __shared__ __align__(16) float xs[DWG_TT][HC];
-  __shared__ __align__(16) float ds[DWG_TT][EMAX];
-  const int hq = threadIdx.x & 63, jg = threadIdx.x >> 6;
-  const int h0 = blockIdx.x * HC;
+  constexpr int JT = EMAX < 8 ? EMAX : 8;
+  constexpr int JG = EMAX / JT;
+  constexpr int HQ = (256 / JG) < 64 ? (256 / JG) : 64;  // threads along h
+  constexpr int NT = HQ * JG;                              // threads per CTA
+  constexpr int HB = HQ * 8;                               // h per CTA
+  __shared__ __align__(16) float xs[DWG_TT][HB];
+  __shared__ __align__(16) float2 ds[DWG_TT][EMAX];
+  const int hq = threadIdx.x % HQ, jg = threadIdx.x / HQ;
+  const int hbase = blockIdx.x * HB;
   const int64_t t_begin = (int64_t)blockIdx.y * tok_per_split;
   int64_t t_end = t_begin + tok_per_split;
   if (t_end > T) t_end = T;
-  float acc[4][EJ];
+  float2 acc[4][JT];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int j = 0; j < EJ; ++j) acc[a][j] = 0.f;
-  for (int64_t tb = t_begin; tb < t_end; tb += DWG_TT) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < DWG_TT * (HC / 8); i += 256) {
-      const int tt = i / (HC / 8), v = i % (HC / 8);
-      const int64_t t = tb + tt;
-      const int h = h0 + v * 8;
-      float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (t < t_end && h < H) {
-        const uint4 u = ld_nc_v4(x + (size_t)t * H + h);
-        float2 a0 = unpack_bf16x2(u.x), a1 = unpack_bf16x2(u.y), a2 = unpack_bf16x2(u.z),
-               a3 = unpack_bf16x2(u.w);
-        f[0] = a0.x; f[1] = a0.y; f[2] = a1.x; f[3] = a1.y;
-        f[4] = a2.x; f[5] = a2.y; f[6] = a3.x; f[7] = a3.y;
-      }
+    for (int j = 0; j < JT; ++j) acc[a][j] = make_float2(0.f, 0.f);
+  // register-staged double buffering: the next tile's x / dl loads are in flight
+  // while the current tile is consumed from shared memory
+  constexpr int XV = (DWG_TT * HQ + NT - 1) / NT;
+  constexpr int DV = (DWG_TT * EMAX + NT - 1) / NT;
+  uint4 xr[XV];
+  float dr[DV];
+  auto load_tile = [&](int64_t tb) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) xs[tt][v * 8 + k] = f[k];
+    for (int k = 0; k < XV; ++k) {
+      const int i = threadIdx.x + k * NT;
+      const int tt = i / HQ, v = i % HQ;
+      const int64_t t = tb + tt;
+      const int h = hbase + v * 8;
+      xr[k] = (i < DWG_TT * HQ && t < t_end && h < H) ? ld_nc_v4(x + (size_t)t * H + h)
+                                                        : make_uint4(0, 0, 0, 0);
     }
-    for (int i = threadIdx.x; i < DWG_TT * EMAX; i += 256) {
+#pragma unroll
+    for (int k = 0; k < DV; ++k) {
+      const int i = threadIdx.x + k * NT;
       const int tt = i / EMAX, j = i % EMAX;
       const int64_t t = tb + tt;
-      ds[tt][j] = (t < t_end && j < E) ? dl[(size_t)t * E + j] : 0.f;
+      dr[k] = (i < DWG_TT * EMAX && t < t_end && j < E) ? dl[(size_t)t * E + j] : 0.f;
+    }
+  };
+  if (t_begin < t_end) load_tile(t_begin);
+  for (int64_t tb = t_begin; tb < t_end; tb += DWG_TT) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < XV; ++k) {
+      const int i = threadIdx.x + k * NT;
+      if (i >= DWG_TT * HQ) continue;
+      const int tt = i / HQ, v = i % HQ;
+      const float2 a0 = unpack_bf16x2(xr[k].x), a1 = unpack_bf16x2(xr[k].y),
+                   a2 = unpack_bf16x2(xr[k].z), a3 = unpack_bf16x2(xr[k].w);
+      *reinterpret_cast<float4*>(&xs[tt][v * 4]) = make_float4(a0.x, a0.y, a1.x, a1.y);
+      *reinterpret_cast<float4*>(&xs[tt][HB / 2 + v * 4]) = make_float4(a2.x, a2.y, a3.x, a3.y);
+    }
+#pragma unroll
+    for (int k = 0; k < DV; ++k) {
+      const int i = threadIdx.x + k * NT;
+      if (i < DWG_TT * EMAX) ds[i / EMAX][i % EMAX] = make_float2(dr[k], dr[k]);
     }
     __syncthreads();
-#pragma unroll 4
+    if (tb + DWG_TT < t_end) load_tile(tb + DWG_TT);
+#pragma unroll 2
     for (int tt = 0; tt < DWG_TT; ++tt) {
-      const float4 xv = *reinterpret_cast<const float4*>(&xs[tt][hq * 4]);
-      float dv[EJ];
+      const float4 xa = *reinterpret_cast<const float4*>(&xs[tt][hq * 4]);
+      const float4 xb = *reinterpret_cast<const float4*>(&xs[tt][HB / 2 + hq * 4]);
+      const float2 x0 = make_float2(xa.x, xa.y), x1 = make_float2(xa.z, xa.w);
+      const float2 x2 = make_float2(xb.x, xb.y), x3 = make_float2(xb.z, xb.w);
 #pragma unroll
-      for (int j = 0; j < EJ; ++j) dv[j] = ds[tt][jg * EJ + j];
-#pragma unroll
-      for (int j = 0; j < EJ; ++j) {
-        acc[0][j] = fmaf(xv.x, dv[j], acc[0][j]);
-        acc[1][j] = fmaf(xv.y, dv[j], acc[1][j]);
-        acc[2][j] = fmaf(xv.z, dv[j], acc[2][j]);
-        acc[3][j] = fmaf(xv.w, dv[j], acc[3][j]);
+      for (int j = 0; j < JT; ++j) {
+        const float2 d = ds[tt][jg * JT + j];
+        ffma2(acc[0][j], x0, d);
+        ffma2(acc[1][j], x1, d);
+        ffma2(acc[2][j], x2, d);
+        ffma2(acc[3][j], x3, d);
       }
     }
   }
+  const int h = hbase + hq * 8;
+  if (h >= H) return;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int h = h0 + hq * 4 + a;
-    if (h >= H) continue;
+  for (int j = 0; j < JT; ++j) {
+    const int jj = jg * JT + j;
+    if (jj >= E) continue;
+    float* dst = partial + ((size_t)blockIdx.y * H + h) * E + jj;
 #pragma unroll
-    for (int j = 0; j < EJ; ++j) {
-      const int jj = jg * EJ + j;
-      if (jj < E) partial[((size_t)blockIdx.y * H + h) * E + jj] = acc[a][j];
+    for (int a = 0; a < 4; ++a) {
+      dst[(size_t)(2 * a) * E] = acc[a][j].x;
+      dst[(size_t)(2 * a + 1) * E] = acc[a][j].y;
     }
   }
 }
@@ -352,28 +406,40 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ partial, int nsplit,
   dwg[i] = s;
 }
 
-template <int EMAX, int TPW>
+int g_sms = 0;
+
+template <int EMAX, int TPW, int GW>
 cudaError_t launch_gate_bwd(const void* x, const void* dS, const float* wg, const float* logits,
                             const int32_t* expert, const int32_t* slot, const float* prob,
                             const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                             float* dl, float* partial, int nsplit, cudaStream_t s) {
-  const int64_t per_cta = (int64_t)WARPS * TPW;
-  const unsigned grid = (unsigned)((T + per_cta - 1) / per_cta);
-  const int smem = EMAX * HC * 4;
+  constexpr int hmax = wg_chunk(EMAX);
+  const int hch = ss.H < hmax ? ss.H : hmax;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_kernel<EMAX, TPW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_kernel<EMAX, TPW, GW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gate_bwd_dx_kernel<EMAX, TPW><<<grid, WARPS * 32, smem, s>>>(
-      static_cast<const bf16*>(dS), wg, logits, expert, slot, prob, dp, ss, T,
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t per_cta = (int64_t)GW * 4 * TPW;
+  int64_t grid = (T + per_cta - 1) / per_cta;
+  if (hch >= ss.H && grid > g_sms) grid = g_sms;
+  gate_bwd_dx_kernel<EMAX, TPW, GW><<<(unsigned)grid, GW * 32, EMAX * hch * 4, s>>>(
+      static_cast<const bf16*>(dS), wg, logits, expert, slot, prob, dp, ss, T, hch,
       static_cast<bf16*>(dx), dl);
-  const int64_t tps = ((T + nsplit - 1) / nsplit + DWG_TT - 1) / DWG_TT * DWG_TT;
   constexpr int EM = EMAX < 4 ? 4 : EMAX;
-  dim3 g2((ss.H + HC - 1) / HC, nsplit);
-  dwg_partial_kernel<EM><<<g2, 256, 0, s>>>(static_cast<const bf16*>(x), dl, T, ss.H, ss.E, tps,
+  constexpr int JT = EM < 8 ? EM : 8;
+  constexpr int HQ = (256 / (EM / JT)) < 64 ? (256 / (EM / JT)) : 64;
+  constexpr int HB = HQ * 8;
+  const int64_t tps = ((T + nsplit - 1) / nsplit + DWG_TT - 1) / DWG_TT * DWG_TT;
+  dim3 g2((ss.H + HB - 1) / HB, nsplit);
+  dwg_partial_kernel<EM><<<g2, HQ * (EM / JT), 0, s>>>(static_cast<const bf16*>(x), dl, T, ss.H, ss.E, tps,
                                             partial);
   const int64_t n = (int64_t)ss.H * ss.E;
   dwg_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(partial, nsplit, n, dwg);
@@ -385,9 +451,9 @@ inline unsigned blocks_for(int64_t n) { return (unsigned)((n + WARPS - 1) / WARP
 }  // namespace
 
 int gate_bwd_splits(int64_t T) {
-  int64_t s = T / 512;
+  int64_t s = T / 128;
   if (s < 1) s = 1;
-  if (s > 32) s = 32;
+  if (s > 128) s = 128;
   return (int)s;
 }
 
@@ -428,13 +494,13 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                      float* dl_scratch, float* dwg_partial, int nsplit, cudaStream_t s) {
   if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * ss.H * ss.E, s);
-#define GB(EM, TP) \
-  launch_gate_bwd<EM, TP>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, s)
-  if (ss.E <= 4) return GB(4, 8);
-  if (ss.E <= 8) return GB(8, 8);
-  if (ss.E <= 16) return GB(16, 4);
-  if (ss.E <= 32) return GB(32, 2);
-  return GB(64, 1);
+#define GB(EM, TP, GW) \
+  launch_gate_bwd<EM, TP, GW>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, s)
+  if (ss.E <= 4) return GB(4, 2, 16);
+  if (ss.E <= 8) return GB(8, 2, 16);
+  if (ss.E <= 16) return GB(16, 1, 16);
+  if (ss.E <= 32) return GB(32, 1, 16);
+  return GB(64, 1, 8);
 #undef GB
 }
 

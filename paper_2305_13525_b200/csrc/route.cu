@@ -1,13 +1,13 @@
 // route.cu — F1 (top-1 gate) and F2 (capacity slot scan), SURVEY §8(a).
 //
 // F1 gate: l = x Wg with fp32 accumulation, softmax max/denominator, lowest-index
-// argmax, top-2 gap, p = softmax(l)[e*] (R1, R4). One warp owns TPW
-// tokens at a time; lane l handles h = 8 l + 256 i + j, so each lane loads one
-// 16-byte vector of x per 256-wide H step (fully coalesced), and the matching
-// Wg values come from a shared-memory copy laid out so the two LDS.128 per
-// (e, i) are conflict-free across the warp. Partial sums per lane cover H/32
-// terms, then a butterfly reduce: a tree summation whose error (~1e-7 on N(0,1)
-// logits) stays well below the 1e-6 tie threshold of BASELINE.json.
+// argmax, top-2 gap, p = softmax(l)[e*] (R1, R4). The contraction is
+// ALU-bound on CUDA cores (E flop/byte): Wg sits in shared memory
+// (resident when H*E*4 <= 128 KiB, else streamed per H-chunk), each 128 B Wg line
+// feeds 4 tokens by broadcast, and the FMAs are packed fma.rn.f32x2. Every lane
+// sums H/8 terms in two (even/odd) chains and the 8 lanes of a token are combined
+// by a fixed xor tree: error ~1e-7 on N(0,1) logits, well below the 1e-6 tie
+// threshold of BASELINE.json.
 //
 // F2 slots: slot_t = #{t' < t : e*(t') = e*(t)} (R3), in two passes over
 // 1024-token blocks: (a) per-block warp-match ranks + block histogram,
@@ -21,83 +21,112 @@
 namespace moe {
 namespace {
 
-constexpr int GATE_WARPS = 8;
-constexpr int HC = 256;  // H chunk staged in shared memory per pass
 
-template <int EMAX, int TPW>
-__global__ void __launch_bounds__(GATE_WARPS * 32)
+// One CTA = GATE_WARPS warps; a warp = 4 token groups (q = lane / 8) of 8 lanes (l8) that
+// split H: lane l8 owns h = 64 blk + 8 l8 + [0, 8) of every 64-wide step. Each
+// lane carries TPW tokens (token = base + 4 i + q), so a warp holds 4*TPW tokens.
+// Accumulators are float2 (even h, odd h) updated with fma.rn.f32x2; the final
+// sum is (even + odd) then a 3-level xor-shuffle over the 8 lanes.
+template <int EMAX, int TPW, int GATE_WARPS>
+__global__ void __launch_bounds__(GATE_WARPS * 32, 1)
     gate_kernel(const bf16* __restrict__ x, const float* __restrict__ wg,
-                const int32_t* __restrict__ forced, int64_t T, int H, int E,
+                const int32_t* __restrict__ forced, int64_t T, int H, int E, int hch,
                 float* __restrict__ logits, int32_t* __restrict__ expert,
                 float* __restrict__ prob, float* __restrict__ gap, int32_t* __restrict__ ties) {
-  // ws[e][HC] permuted: h_local = 8 l + 4 half + q  ->  e*HC + half*128 + l*4 + q
-  extern __shared__ __align__(16) float ws[];  // [EMAX * HC]
+  extern __shared__ __align__(16) float ws[];  // [EMAX][hch], see ws_index
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tok0 = ((int64_t)blockIdx.x * GATE_WARPS + warp) * TPW;
-
-  float acc[TPW][EMAX];
-#pragma unroll
-  for (int t = 0; t < TPW; ++t)
-#pragma unroll
-    for (int e = 0; e < EMAX; ++e) acc[t][e] = 0.f;
-
-  for (int h0 = 0; h0 < H; h0 += HC) {
+  const int q = lane >> 3, l8 = lane & 7;
+  constexpr int PER_WARP = 4 * TPW;
+  constexpr int PER_CTA = GATE_WARPS * PER_WARP;
+  constexpr int PD = EMAX >= 64 ? 2 : 4;  // x prefetch depth (64-wide H steps)
+  const int nchunks = (H + hch - 1) / hch;
+  const bool resident = nchunks == 1;
+  if (resident) {
+    stage_wg(ws, wg, 0, hch, H, E);
     __syncthreads();
-    for (int i = threadIdx.x; i < EMAX * HC; i += blockDim.x) {
-      const int e = i / HC, hl = i % HC;
-      const int l = hl >> 3, half = (hl >> 2) & 1, q = hl & 3;
-      const int h = h0 + hl;
-      ws[e * HC + half * 128 + l * 4 + q] = (e < E && h < H) ? wg[(size_t)h * E + e] : 0.f;
-    }
-    __syncthreads();
-    const int h = h0 + 8 * lane;
-    if (h < H) {
-      float xv[TPW][8];
+  }
+  const int64_t nbatch = (T + PER_CTA - 1) / PER_CTA;
+  for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+    const int64_t base = b * PER_CTA + warp * PER_WARP + q;
+    float2 acc[TPW][EMAX];
 #pragma unroll
-      for (int t = 0; t < TPW; ++t) {
-        const int64_t tok = tok0 + t;
-        uint4 u = make_uint4(0, 0, 0, 0);
-        if (tok < T) u = ld_nc_v4(x + (size_t)tok * H + h);
-        float2 f0 = unpack_bf16x2(u.x), f1 = unpack_bf16x2(u.y), f2 = unpack_bf16x2(u.z),
-               f3 = unpack_bf16x2(u.w);
-        xv[t][0] = f0.x; xv[t][1] = f0.y; xv[t][2] = f1.x; xv[t][3] = f1.y;
-        xv[t][4] = f2.x; xv[t][5] = f2.y; xv[t][6] = f3.x; xv[t][7] = f3.y;
+    for (int i = 0; i < TPW; ++i)
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e) acc[i][e] = make_float2(0.f, 0.f);
+
+    for (int c = 0; c < nchunks; ++c) {
+      const int h0 = c * hch;
+      if (!resident) {
+        __syncthreads();
+        stage_wg(ws, wg, h0, hch, H, E);
+        __syncthreads();
       }
+      const int nblk = (H - h0 < hch ? H - h0 : hch) >> 6;
+      // software pipeline: x for steps blk .. blk+PD-1 in flight (PD*TPW 16-byte loads per lane)
+      uint4 buf[PD][TPW];
 #pragma unroll
-      for (int e = 0; e < EMAX; ++e) {
-        const float4 w0 = *reinterpret_cast<const float4*>(&ws[e * HC + lane * 4]);
-        const float4 w1 = *reinterpret_cast<const float4*>(&ws[e * HC + 128 + lane * 4]);
+      for (int s = 0; s < PD; ++s)
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          float a = acc[t][e];
-          a = fmaf(xv[t][0], w0.x, a); a = fmaf(xv[t][1], w0.y, a);
-          a = fmaf(xv[t][2], w0.z, a); a = fmaf(xv[t][3], w0.w, a);
-          a = fmaf(xv[t][4], w1.x, a); a = fmaf(xv[t][5], w1.y, a);
-          a = fmaf(xv[t][6], w1.z, a); a = fmaf(xv[t][7], w1.w, a);
-          acc[t][e] = a;
+        for (int i = 0; i < TPW; ++i) {
+          const int64_t tok = base + 4 * i;
+          buf[s][i] = (tok < T && s < nblk) ? ld_nc_v4(x + (size_t)tok * H + h0 + 64 * s + 8 * l8)
+                                            : make_uint4(0, 0, 0, 0);
+        }
+      for (int blk0 = 0; blk0 < nblk; blk0 += PD) {
+#pragma unroll
+        for (int s = 0; s < PD; ++s) {
+          const int blk = blk0 + s;
+          if (blk < nblk) {
+            float2 xv[TPW][4];
+#pragma unroll
+            for (int i = 0; i < TPW; ++i) {
+              xv[i][0] = unpack_bf16x2(buf[s][i].x); xv[i][1] = unpack_bf16x2(buf[s][i].y);
+              xv[i][2] = unpack_bf16x2(buf[s][i].z); xv[i][3] = unpack_bf16x2(buf[s][i].w);
+              const int64_t tok = base + 4 * i;
+              if (tok < T && blk + PD < nblk)
+                buf[s][i] = ld_nc_v4(x + (size_t)tok * H + h0 + 64 * (blk + PD) + 8 * l8);
+            }
+            const float* wrow = ws + blk * 64 + l8 * 4;
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e) {
+              const float4 w0 = *reinterpret_cast<const float4*>(wrow + e * hch);
+              const float4 w1 = *reinterpret_cast<const float4*>(wrow + e * hch + 32);
+              const float2 p0 = make_float2(w0.x, w0.y), p1 = make_float2(w0.z, w0.w);
+              const float2 p2 = make_float2(w1.x, w1.y), p3 = make_float2(w1.z, w1.w);
+#pragma unroll
+              for (int i = 0; i < TPW; ++i) {
+                ffma2(acc[i][e], xv[i][0], p0);
+                ffma2(acc[i][e], xv[i][1], p1);
+                ffma2(acc[i][e], xv[i][2], p2);
+                ffma2(acc[i][e], xv[i][3], p3);
+              }
+            }
+          }
         }
       }
     }
-  }
-  // butterfly reduction of the 32 lane partials (fixed tree order)
+    // (even + odd), then tree over the 8 lanes of the token group (result in .x)
 #pragma unroll
-  for (int t = 0; t < TPW; ++t)
+    for (int i = 0; i < TPW; ++i)
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) acc[t][e] = warp_sum(acc[t][e]);
-
-  if (lane < TPW) {
-    // every lane holds every sum; lane t finalises token tok0 + t
+      for (int e = 0; e < EMAX; ++e) {
+        float v = acc[i][e].x + acc[i][e].y;
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        acc[i][e].x = v;
+      }
+    // lane l8 == i finalises token base + 4 i
 #pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      if (t != lane) continue;
-      const int64_t tok = tok0 + t;
-      if (tok >= T) continue;
+    for (int i = 0; i < TPW; ++i) {
+      const int64_t tok = base + 4 * i;
+      if (l8 != i || tok >= T) continue;
       float m = -FLT_MAX, m2 = -FLT_MAX;
       int best = 0;
 #pragma unroll
       for (int e = 0; e < EMAX; ++e) {
         if (e >= E) break;
-        const float v = acc[t][e];
+        const float v = acc[i][e].x;
         logits[(size_t)tok * E + e] = v;
         if (v > m) { m2 = m; m = v; best = e; }
         else if (v > m2) { m2 = v; }
@@ -106,14 +135,13 @@ __global__ void __launch_bounds__(GATE_WARPS * 32)
 #pragma unroll
       for (int e = 0; e < EMAX; ++e) {
         if (e >= E) break;
-        den += expf(acc[t][e] - m);
+        den += expf(acc[i][e].x - m);
       }
-      int chosen = best;
-      if (forced) chosen = forced[tok];
+      const int chosen = forced ? forced[tok] : best;
       float lc = m;
 #pragma unroll
       for (int e = 0; e < EMAX; ++e)
-        if (e == chosen) lc = acc[t][e];
+        if (e == chosen) lc = acc[i][e].x;
       const float g = (E > 1) ? (m - m2) : FLT_MAX;
       expert[tok] = chosen;
       prob[tok] = expf(lc - m) / den;
@@ -186,21 +214,31 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
   }
 }
 
-template <int EMAX, int TPW>
+int g_sms = 0;
+
+template <int EMAX, int TPW, int GATE_WARPS>
 cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
-  const int64_t per_cta = (int64_t)GATE_WARPS * TPW;
-  const int64_t grid = (a.T + per_cta - 1) / per_cta;
-  const int smem = EMAX * HC * 4;
+  constexpr int hmax = wg_chunk(EMAX);
+  const int hch = a.H < hmax ? a.H : hmax;
+  const int smem = EMAX * hch * 4;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gate_kernel<EMAX, TPW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(gate_kernel<EMAX, TPW, GATE_WARPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gate_kernel<EMAX, TPW><<<(unsigned)grid, GATE_WARPS * 32, smem, s>>>(
-      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, a.logits, a.expert, a.prob,
-      a.gap, a.ties);
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t per_cta = (int64_t)GATE_WARPS * 4 * TPW;
+  int64_t grid = (a.T + per_cta - 1) / per_cta;
+  if (hch >= a.H && grid > g_sms) grid = g_sms;  // Wg resident: persistent over token batches
+  gate_kernel<EMAX, TPW, GATE_WARPS><<<(unsigned)grid, GATE_WARPS * 32, smem, s>>>(
+      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, hch, a.logits, a.expert,
+      a.prob, a.gap, a.ties);
   return cudaGetLastError();
 }
 
@@ -214,11 +252,11 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s) {
     if (e == cudaSuccess) e = cudaMemsetAsync(a.load, 0, sizeof(int32_t) * a.E, s);
     return e;
   }
-  if (a.E <= 4) e = launch_gate<4, 8>(a, s);
-  else if (a.E <= 8) e = launch_gate<8, 8>(a, s);
-  else if (a.E <= 16) e = launch_gate<16, 4>(a, s);
-  else if (a.E <= 32) e = launch_gate<32, 2>(a, s);
-  else e = launch_gate<64, 1>(a, s);
+  if (a.E <= 4) e = launch_gate<4, 2, 16>(a, s);
+  else if (a.E <= 8) e = launch_gate<8, 2, 16>(a, s);
+  else if (a.E <= 16) e = launch_gate<16, 1, 16>(a, s);
+  else if (a.E <= 32) e = launch_gate<32, 1, 16>(a, s);
+  else e = launch_gate<64, 1, 8>(a, s);
   if (e != cudaSuccess) return e;
   const int nblocks = (int)((a.T + SCAN_BLOCK - 1) / SCAN_BLOCK);
   slot_local_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.T, a.E, a.local_rank, a.block_hist);
