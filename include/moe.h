@@ -204,8 +204,9 @@ const char* moe_last_error_detail(void);
  *   epilogue 0: D = bf16(acc)
  *   epilogue 1: D = bf16(acc) (Hpre), aux = bf16(gelu_tanh(acc)) [batch][M][N]
  *   epilogue 2: D = bf16(acc * gelu_tanh'(aux)), aux = Hpre bf16 [batch][M][N] (read)
- *   impl 0: tcgen05 kernel (the product path); impl 1: plain SIMT reference
- *   kernel (bring-up cross-check only; never used by moe_forward/backward). */
+ *   impl 0: tcgen05 CTA-pair kernel (cta_group::2, the product path);
+ *   impl 2: tcgen05 single-CTA kernel; impl 1: plain SIMT reference kernel
+ *   (bring-up cross-check only; never used by moe_forward/backward). */
 moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn,
                          const void* B, int b_mn, void* D, int epilogue, void* aux,
                          int impl, void* stream);

@@ -262,6 +262,217 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- 2-CTA variant
+// A CTA pair (cluster of 2) computes a 256 x 256 tile with tcgen05.mma.cta_group::2
+// (M = 256): each CTA stages its 128 rows of A and its 128 rows of B per
+// k-block (32 KiB / stage, 6 stages), so per-SM shared-memory traffic per MMA
+// is halved versus the 1-CTA 128 x 256 tile. The leader (rank 0) issues the
+// MMAs; both CTAs' TMA loads count on the leader's full barrier; commits are
+// multicast to both CTAs; each CTA's epilogue drains its own 128 TMEM lanes and
+// both arrive on the leader's tmem-empty barrier.
+constexpr int STAGES2 = 6;
+constexpr int A2_STAGE = 128 * BK * 2;  // 16 KiB
+constexpr int B2_STAGE = 128 * BK * 2;  // 16 KiB (this CTA's half of BN = 256)
+constexpr int SMEM2_BYTES = STAGES2 * (A2_STAGE + B2_STAGE) + 1024 + 256;
+
+__host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <int A_MN, int B_MN, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES2 * A2_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + STAGES2 * B2_STAGE);
+  // [0,S) full (leader's counts both CTAs), [S,2S) empty, [2S,2S+2) tmem_full, [2S+2,2S+4) tmem_empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(smem_u32(&bars[s]), 1);
+      mbar_init(smem_u32(&bars[STAGES2 + s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
+      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int tiles_mn = p.tiles_m * p.tiles_n;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < p.total_tiles; tile += nclusters) {
+        const int b = tile / tiles_mn;
+        const int r = tile - b * tiles_mn;
+        const int m0 = (r / p.tiles_n) * 256 + rank * 128;
+        const int n0 = (r % p.tiles_n) * BN + rank * 128;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1);
+          const uint32_t full = smem_u32(&bars[stage]);
+          if (leader) mbar_arrive_expect_tx(full, 2 * (A2_STAGE + B2_STAGE));
+          const uint32_t a_dst = smem_u32(smA + stage * A2_STAGE);
+          const uint32_t b_dst = smem_u32(smB + stage * B2_STAGE);
+          const int k0 = kb * BK;
+          if (A_MN) {
+            tma_load_3d_2sm(a_dst, &tmA, full, m0, k0, b);
+            tma_load_3d_2sm(a_dst + 8192, &tmA, full, m0 + 64, k0, b);
+          } else {
+            tma_load_3d_2sm(a_dst, &tmA, full, k0, m0, b);
+          }
+          if (B_MN) {
+            tma_load_3d_2sm(b_dst, &tmB, full, n0, k0, b);
+            tma_load_3d_2sm(b_dst + 8192, &tmB, full, n0 + 64, k0, b);
+          } else {
+            tma_load_3d_2sm(b_dst, &tmB, full, k0, n0, b);
+          }
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = instr_desc_m256(A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = cluster; tile < p.total_tiles; tile += nclusters, ++iter) {
+        const int acc = iter & 1;
+        const uint32_t acc_phase = (iter >> 1) & 1;
+        mbar_wait(smem_u32(&bars[2 * STAGES2 + 2 + acc]), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(smem_u32(&bars[stage]), phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smA + stage * A2_STAGE);
+          const uint32_t b_base = smem_u32(smB + stage * B2_STAGE);
+#pragma unroll
+          for (int j = 0; j < BK / 16; ++j) {
+            const uint64_t ad = A_MN ? smem_desc(a_base + j * 2048, 8192, 1024)
+                                     : smem_desc(a_base + j * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(b_base + j * 2048, 8192, 1024)
+                                     : smem_desc(b_base + j * 32, 16, 1024);
+            tc_mma_f16_2sm(tmem_d, ad, bd, idesc, (kb | j) != 0);
+          }
+          tc_commit_2sm(smem_u32(&bars[STAGES2 + stage]), 0x3);
+          if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm(smem_u32(&bars[2 * STAGES2 + acc]), 0x3);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quad = warp & 3;
+    int iter = 0;
+    for (int tile = cluster; tile < p.total_tiles; tile += nclusters, ++iter) {
+      const int b = tile / tiles_mn;
+      const int r = tile - b * tiles_mn;
+      const int m0 = (r / p.tiles_n) * 256 + rank * 128;
+      const int n0 = (r % p.tiles_n) * BN;
+      const int acc = iter & 1;
+      const uint32_t acc_phase = (iter >> 1) & 1;
+      mbar_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase);
+      tc_fence_after();
+      const int m = m0 + quad * 32 + lane;
+      const bool row_ok = m < p.M;
+      const size_t row_off = ((size_t)b * p.M + (row_ok ? m : 0)) * (size_t)p.N;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c, v);
+        tmem_wait_ld();
+        const int n = n0 + c;
+        if (row_ok && n < p.N) {
+          bf16* dst = p.D + row_off + n;
+          if (EPI == EPI_DGELU) {
+            const bf16* hsrc = p.aux + row_off + n;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 h = *reinterpret_cast<const uint4*>(hsrc + q * 8);
+              uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+              uint32_t o[4];
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                float2 hv = unpack_bf16x2(hw[w]);
+                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]) * gelu_grad_f(hv.x),
+                                   __uint_as_float(v[q * 8 + 2 * w + 1]) * gelu_grad_f(hv.y));
+              }
+              st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t o[4];
+#pragma unroll
+              for (int w = 0; w < 4; ++w)
+                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]),
+                                   __uint_as_float(v[q * 8 + 2 * w + 1]));
+              st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
+            }
+            if (EPI == EPI_GELU) {
+              bf16* adst = p.aux + row_off + n;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t o[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                  o[w] = pack_bf16x2(gelu_f(__uint_as_float(v[q * 8 + 2 * w])),
+                                     gelu_f(__uint_as_float(v[q * 8 + 2 * w + 1])));
+                st_v4(adst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(smem_u32(&bars[2 * STAGES2 + 2 + acc]), 0);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 int g_num_sms = 0;
@@ -307,37 +518,75 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
   return cudaGetLastError();
 }
 
+template <int A_MN, int B_MN, int EPI>
+cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
+  static bool attr = false;
+  auto k = gemm2_kernel<A_MN, B_MN, EPI>;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int clusters = g_num_sms / 2;
+  if (p.total_tiles < clusters) clusters = p.total_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM2_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, ta, tb, p);
+}
+
 }  // namespace
 
 cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   std::call_once(g_once, init_once);
   if (g_init_err != cudaSuccess) { *why = "driver entry point / device query failed"; return g_init_err; }
   if (a.batch <= 0 || a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaSuccess;
+  const bool pair = a.variant != 1;  // default: CTA-pair (cta_group::2) kernel
   CUtensorMap ta, tb;
   bool ok = a.a_mn ? make_map(&ta, a.A, a.M, a.K, a.batch, 64, 64)
                    : make_map(&ta, a.A, a.K, a.M, a.batch, 64, BM);
   ok = ok && (a.b_mn ? make_map(&tb, a.B, a.N, a.K, a.batch, 64, 64)
-                     : make_map(&tb, a.B, a.K, a.N, a.batch, 64, BN));
+                     : make_map(&tb, a.B, a.K, a.N, a.batch, 64, pair ? 128 : BN));
   if (!ok) { *why = "cuTensorMapEncodeTiled rejected the operand layout"; return cudaErrorInvalidValue; }
   Params p;
   p.batch = a.batch; p.M = a.M; p.N = a.N; p.K = a.K;
-  p.tiles_m = (a.M + BM - 1) / BM;
+  p.tiles_m = (a.M + (pair ? 256 : BM) - 1) / (pair ? 256 : BM);
   p.tiles_n = (a.N + BN - 1) / BN;
   p.total_tiles = p.tiles_m * p.tiles_n * a.batch;
   p.k_blocks = (a.K + BK - 1) / BK;
   p.D = static_cast<bf16*>(a.D);
   p.aux = static_cast<bf16*>(a.aux);
   const int key = a.a_mn * 100 + a.b_mn * 10 + a.epilogue;
-  switch (key) {
-    case 0:   return launch<0, 0, EPI_STORE>(ta, tb, p, s);
-    case 1:   return launch<0, 0, EPI_GELU>(ta, tb, p, s);
-    case 10:  return launch<0, 1, EPI_STORE>(ta, tb, p, s);
-    case 12:  return launch<0, 1, EPI_DGELU>(ta, tb, p, s);
-    case 110: return launch<1, 1, EPI_STORE>(ta, tb, p, s);
-    default:
-      *why = "operand-major / epilogue combination not instantiated";
-      return cudaErrorNotSupported;
+  if (pair) {
+    switch (key) {
+      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, p, s);
+      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, p, s);
+      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, p, s);
+      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, p, s);
+      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, p, s);
+      default: break;
+    }
+  } else {
+    switch (key) {
+      case 0:   return launch<0, 0, EPI_STORE>(ta, tb, p, s);
+      case 1:   return launch<0, 0, EPI_GELU>(ta, tb, p, s);
+      case 10:  return launch<0, 1, EPI_STORE>(ta, tb, p, s);
+      case 12:  return launch<0, 1, EPI_DGELU>(ta, tb, p, s);
+      case 110: return launch<1, 1, EPI_STORE>(ta, tb, p, s);
+      default: break;
+    }
   }
+  *why = "operand-major / epilogue combination not instantiated";
+  return cudaErrorNotSupported;
 }
 
 // ---------------------------------------------------------------- SIMT reference

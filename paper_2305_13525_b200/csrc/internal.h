@@ -19,6 +19,7 @@ struct GemmArgs {
   void* D;   // [b][M][N]
   int epilogue;
   void* aux;  // EPI_GELU: out [b][M][N]; EPI_DGELU: in (Hpre) [b][M][N]
+  int variant = 0;  // 0: CTA-pair kernel (cta_group::2, product path); 1: single-CTA kernel
 };
 
 // tcgen05 / TMEM / TMA kernel (the product path).
