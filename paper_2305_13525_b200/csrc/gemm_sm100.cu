@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 constexpr int STAGES2 = 6;
 constexpr int A2_STAGE = 128 * BK * 2;  // 16 KiB
 constexpr int B2_STAGE = 128 * BK * 2;  // 16 KiB (this CTA's half of BN = 256)
-constexpr int SMEM2_BYTES = STAGES2 * (A2_STAGE + B2_STAGE) + 1024 + 256;
+constexpr int EPI_BUF = 32 * 32 * 2;  // one warp's 32 x 32 bf16 chunk, 64B-swizzled
+// per epilogue warp: 2 buffers for D and 2 for the GeLU output
+constexpr int EPI_SMEM = 4 * 4 * EPI_BUF;  // 32 KiB
+constexpr int SMEM2_BYTES = STAGES2 * (A2_STAGE + B2_STAGE) + EPI_SMEM + 1024 + 256;
 
 __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
@@ -283,13 +286,15 @@ __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
 template <int A_MN, int B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                  const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES2 * A2_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + STAGES2 * B2_STAGE);
+  uint8_t* smE = smB + STAGES2 * B2_STAGE;  // epilogue staging (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smE + EPI_SMEM);
   // [0,S) full (leader's counts both CTAs), [S,2S) empty, [2S,2S+2) tmem_full, [2S+2,2S+4) tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
 
@@ -303,6 +308,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmD);
+    if (EPI == EPI_GELU) tma_prefetch_desc(&tmX);
     for (int s = 0; s < STAGES2; ++s) {
       mbar_init(smem_u32(&bars[s]), 1);
       mbar_init(smem_u32(&bars[STAGES2 + s]), 1);
@@ -395,8 +402,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
+    // TMEM -> registers -> (epilogue math) -> bf16 -> 64B-swizzled smem chunk of
+    // 32 rows x 32 cols -> TMA bulk-tensor store (coalesced; rows >= M and
+    // columns >= N are clipped by the tensor map). Two buffers per output per
+    // warp; a buffer is rewritten only after its previous store has been read.
     const int quad = warp & 3;
-    int iter = 0;
+    const uint32_t ebase = smem_u32(smE) + quad * 4 * EPI_BUF;
+    const uint32_t swz = (uint32_t)((lane >> 1) & 3);
+    int iter = 0, chunk_ctr = 0;
     for (int tile = cluster; tile < p.total_tiles; tile += nclusters, ++iter) {
       const int b = tile / tiles_mn;
       const int r = tile - b * tiles_mn;
@@ -406,61 +419,64 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (iter >> 1) & 1;
       mbar_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase);
       tc_fence_after();
-      const int m = m0 + quad * 32 + lane;
+      const int mrow0 = m0 + quad * 32;
+      const int m = mrow0 + lane;
       const bool row_ok = m < p.M;
       const size_t row_off = ((size_t)b * p.M + (row_ok ? m : 0)) * (size_t)p.N;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
+        const int n = n0 + c;
+        if (n >= p.N) break;  // uniform across the warp
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c, v);
+        uint4 hpre[4];
+        if (EPI == EPI_DGELU) {
+          const bf16* hsrc = p.aux + row_off + n;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            hpre[q] = row_ok ? *reinterpret_cast<const uint4*>(hsrc + q * 8) : make_uint4(0, 0, 0, 0);
+        }
         tmem_wait_ld();
-        const int n = n0 + c;
-        if (row_ok && n < p.N) {
-          bf16* dst = p.D + row_off + n;
+        uint32_t o[16], g[16];
+#pragma unroll
+        for (int w = 0; w < 16; ++w) {
+          const float f0 = __uint_as_float(v[2 * w]), f1 = __uint_as_float(v[2 * w + 1]);
           if (EPI == EPI_DGELU) {
-            const bf16* hsrc = p.aux + row_off + n;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 h = *reinterpret_cast<const uint4*>(hsrc + q * 8);
-              uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-              uint32_t o[4];
-#pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                float2 hv = unpack_bf16x2(hw[w]);
-                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]) * gelu_grad_f(hv.x),
-                                   __uint_as_float(v[q * 8 + 2 * w + 1]) * gelu_grad_f(hv.y));
-              }
-              st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
-            }
+            const uint32_t hw = (w & 3) == 0 ? hpre[w >> 2].x : (w & 3) == 1 ? hpre[w >> 2].y
+                              : (w & 3) == 2 ? hpre[w >> 2].z : hpre[w >> 2].w;
+            const float2 hv = unpack_bf16x2(hw);
+            o[w] = pack_bf16x2(f0 * gelu_grad_f(hv.x), f1 * gelu_grad_f(hv.y));
           } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t o[4];
-#pragma unroll
-              for (int w = 0; w < 4; ++w)
-                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]),
-                                   __uint_as_float(v[q * 8 + 2 * w + 1]));
-              st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
-            }
-            if (EPI == EPI_GELU) {
-              bf16* adst = p.aux + row_off + n;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t o[4];
-#pragma unroll
-                for (int w = 0; w < 4; ++w)
-                  o[w] = pack_bf16x2(gelu_f(__uint_as_float(v[q * 8 + 2 * w])),
-                                     gelu_f(__uint_as_float(v[q * 8 + 2 * w + 1])));
-                st_v4(adst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
-              }
-            }
+            o[w] = pack_bf16x2(f0, f1);
+            if (EPI == EPI_GELU) g[w] = pack_bf16x2(gelu_f(f0), gelu_f(f1));
           }
+        }
+        const int bi = chunk_ctr & 1;
+        ++chunk_ctr;
+        if (lane == 0) bulk_wait_read_1();
+        __syncwarp();
+        const uint32_t bufD = ebase + bi * EPI_BUF;
+        const uint32_t bufX = ebase + (2 + bi) * EPI_BUF;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t off = lane * 64 + ((q ^ swz) << 4);
+          st_shared_v4(bufD + off, o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          if (EPI == EPI_GELU) st_shared_v4(bufX + off, g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmD, bufD, n, mrow0, b);
+          if (EPI == EPI_GELU) tma_store_3d(&tmX, bufX, n, mrow0, b);
+          bulk_commit();
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(smem_u32(&bars[2 * STAGES2 + 2 + acc]), 0);
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
 
   tc_fence_before();
@@ -491,15 +507,16 @@ void init_once() {
     g_init_err = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
 }
 
-// 3-D bf16 tensor map {inner, outer, batch}, box {box_inner, box_outer, 1}, 128B swizzle.
+// 3-D bf16 tensor map {inner, outer, batch}, box {box_inner, box_outer, 1}.
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t batch,
-              uint32_t box_inner, uint32_t box_outer) {
+              uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   cuuint64_t dims[3] = {inner, outer, batch};
   cuuint64_t strides[2] = {inner * 2, inner * outer * 2};
   cuuint32_t box[3] = {box_inner, box_outer, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
-                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -519,7 +536,8 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
 }
 
 template <int A_MN, int B_MN, int EPI>
-cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
+cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+                    const CUtensorMap& tx, const Params& p, cudaStream_t s) {
   static bool attr = false;
   auto k = gemm2_kernel<A_MN, B_MN, EPI>;
   if (!attr) {
@@ -541,7 +559,7 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& 
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, ta, tb, p);
+  return cudaLaunchKernelEx(&cfg, k, ta, tb, td, tx, p);
 }
 
 }  // namespace
@@ -567,12 +585,18 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   p.aux = static_cast<bf16*>(a.aux);
   const int key = a.a_mn * 100 + a.b_mn * 10 + a.epilogue;
   if (pair) {
+    CUtensorMap td, tx;
+    bool okd = make_map(&td, a.D, a.N, a.M, a.batch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    okd = okd && (a.epilogue != EPI_GELU ||
+                  make_map(&tx, a.aux, a.N, a.M, a.batch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
+    if (a.epilogue != EPI_GELU) tx = td;
+    if (!okd) { *why = "cuTensorMapEncodeTiled rejected the output layout"; return cudaErrorInvalidValue; }
     switch (key) {
-      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, p, s);
-      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, p, s);
-      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, p, s);
-      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, p, s);
-      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, p, s);
+      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, td, tx, p, s);
+      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, td, tx, p, s);
+      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, td, tx, p, s);
+      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, td, tx, p, s);
+      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, td, tx, p, s);
       default: break;
     }
   } else {

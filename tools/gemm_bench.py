@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--config", default="1.3b")
     ap.add_argument("--impl", type=int, nargs="+", default=[0, 2])
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
     sh = synth.CONFIGS[a.config]
     El = sh.experts // sh.g_expert
@@ -49,7 +50,7 @@ def main():
             Mm, Nn = D.shape[1], D.shape[2]
             K = Aop.shape[1] if amn else Aop.shape[2]
             flops = 2.0 * El * Mm * Nn * K
-            for _ in range(3):
+            for _ in range(a.warmup):
                 moe_gemm_bf16(Aop, Bop, D, amn, bmn, epi, aux, impl)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
