@@ -173,18 +173,18 @@ __device__ __forceinline__ void ffma2(float2& d, const float2 a, const float2 b)
 }
 
 // ---------------------------------------------------------------- gate weight staging
-// Wg [H][E] fp32 is staged in shared memory per H-chunk of `hch` (multiple of 64)
-// as ws[e][blk][half][l8][4] with h_local = 64 blk + 8 l8 + 4 half + q, so the
-// 8 lanes of a token group read one contiguous 128 B line per LDS.128 and the
-// four token groups of the warp share it by broadcast.
+// Wg [H][E] fp32 is staged in shared memory per H-chunk of `hch` (multiple of 256)
+// as ws[e][blk][half][lane][4] with h_local = 256 blk + 8 lane + 4 half + q: the
+// two LDS.128 a warp issues per (e, blk) read 512 contiguous bytes each (4
+// wavefronts, no bank conflicts), and lane `lane` receives Wg[h][e] for exactly
+// the 8 h values of its 16-byte x vector.
 __device__ __forceinline__ int ws_index(int e, int hl, int hch) {
-  const int blk = hl >> 6, r = hl & 63, l8 = r >> 3, half = (r >> 2) & 1, q = r & 3;
-  return e * hch + blk * 64 + half * 32 + l8 * 4 + q;
+  const int blk = hl >> 8, r = hl & 255, ln = r >> 3, half = (r >> 2) & 1, q = r & 3;
+  return e * hch + blk * 256 + half * 128 + ln * 4 + q;
 }
 
 // Coalesced over the global [H][E] array; entries for h >= H are zero. 16 loads
-// per thread are issued before their shared-memory stores (one dependent L2
-// round trip per 16 elements instead of per element).
+// per thread are issued before their shared-memory stores.
 __device__ __forceinline__ void stage_wg(float* ws, const float* __restrict__ wg, int h0, int hch,
                                          int H, int E) {
   constexpr int U = 16;
@@ -210,8 +210,8 @@ __device__ __forceinline__ void stage_wg(float* ws, const float* __restrict__ wg
   }
 }
 
-// Largest multiple of 64 with hch * emax * 4 <= 128 KiB.
-__host__ __device__ constexpr int wg_chunk(int emax) { return (128 * 1024 / (emax * 4)) & ~63; }
+// Largest multiple of 256 with hch * emax * 4 <= 128 KiB.
+__host__ __device__ constexpr int wg_chunk(int emax) { return (128 * 1024 / (emax * 4)) & ~255; }
 
 }  // namespace moe
 

@@ -14,7 +14,6 @@ namespace moe {
 namespace {
 
 constexpr int WARPS = 8;
-constexpr int PD = 4;  // prefetch depth (64-wide H steps) of the gate-backward pipeline
 
 __device__ __forceinline__ size_t slot_row(const SlotSpace& ss, int e, int64_t c) {
   const int64_t tt = c / ss.Cs, cs = c - tt * ss.Cs;
@@ -173,8 +172,8 @@ __global__ void __launch_bounds__(WARPS * 32)
 
 // ---------------------------------------------------------------- B10 gate backward
 // dx_t = dS[row(t)] + sum_j dl_tj Wg[h, j]; dl_tj = dp_t p_t (delta_{j e*} - s_tj).
-// Same lane layout and Wg staging as the forward gate (route.cu): 4 token groups
-// of 8 lanes per warp, TPW tokens per lane, packed fma.rn.f32x2 over h pairs.
+// Same structure as the forward gate (route.cu): a warp owns TPW tokens, lane l
+// covers h = 256 i + 8 l + [0, 8), Wg from shared memory reused TPW times.
 template <int EMAX, int TPW, int GW>
 __global__ void __launch_bounds__(GW * 32, 1)
     gate_bwd_dx_kernel(const bf16* __restrict__ dS, const float* __restrict__ wg,
@@ -184,10 +183,8 @@ __global__ void __launch_bounds__(GW * 32, 1)
                        bf16* __restrict__ dx, float* __restrict__ dl_out) {
   extern __shared__ __align__(16) float ws[];  // [EMAX][hch], see ws_index
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = lane >> 3, l8 = lane & 7;
   const int E = ss.E, H = ss.H;
-  constexpr int PER_WARP = 4 * TPW;
-  constexpr int PER_CTA = GW * PER_WARP;
+  constexpr int PER_CTA = GW * TPW;
   const int nchunks = (H + hch - 1) / hch;
   const bool resident = nchunks == 1;
   if (resident) {
@@ -196,22 +193,21 @@ __global__ void __launch_bounds__(GW * 32, 1)
   }
   const int64_t nbatch = (T + PER_CTA - 1) / PER_CTA;
   for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
-    const int64_t base = b * PER_CTA + warp * PER_WARP + q;
-    float2 dl2[TPW][EMAX];  // (dl, dl) pairs
+    const int64_t tok0 = b * PER_CTA + warp * TPW;
+    float dl[TPW][EMAX];
     size_t row[TPW];
     bool kept[TPW], valid[TPW];
 #pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-      const int64_t tok = base + 4 * i;
-      valid[i] = tok < T;
-      kept[i] = valid[i] && slot[tok] >= 0;
-      row[i] = 0;
-      float d[EMAX];
+    for (int t = 0; t < TPW; ++t) {
+      const int64_t tok = tok0 + t;
+      valid[t] = tok < T;
+      kept[t] = valid[t] && slot[tok] >= 0;
+      row[t] = 0;
 #pragma unroll
-      for (int j = 0; j < EMAX; ++j) d[j] = 0.f;
-      if (kept[i]) {
+      for (int j = 0; j < EMAX; ++j) dl[t][j] = 0.f;
+      if (kept[t]) {
         const int e = expert[tok];
-        row[i] = slot_row(ss, e, slot[tok]);
+        row[t] = slot_row(ss, e, slot[tok]);
         float m = -3.402823e38f;
 #pragma unroll
         for (int j = 0; j < EMAX; ++j)
@@ -220,21 +216,29 @@ __global__ void __launch_bounds__(GW * 32, 1)
 #pragma unroll
         for (int j = 0; j < EMAX; ++j)
           if (j < E) {
-            d[j] = expf(logits[(size_t)tok * E + j] - m);
-            den += d[j];
+            dl[t][j] = expf(logits[(size_t)tok * E + j] - m);
+            den += dl[t][j];
           }
         const float g = dp[tok] * prob[tok];
         const float inv = 1.0f / den;
 #pragma unroll
-        for (int j = 0; j < EMAX; ++j) d[j] = j < E ? g * ((j == e ? 1.f : 0.f) - d[j] * inv) : 0.f;
+        for (int j = 0; j < EMAX; ++j)
+          dl[t][j] = j < E ? g * ((j == e ? 1.f : 0.f) - dl[t][j] * inv) : 0.f;
       }
-      if (valid[i] && l8 == 0) {
+      if (valid[t] && lane < E) {
+        float v = 0.f;
 #pragma unroll
         for (int j = 0; j < EMAX; ++j)
-          if (j < E) dl_out[(size_t)tok * E + j] = d[j];
+          if (j == lane) v = dl[t][j];
+        dl_out[(size_t)tok * E + lane] = v;
       }
+      if (EMAX > 32 && valid[t] && lane + 32 < E) {
+        float v = 0.f;
 #pragma unroll
-      for (int j = 0; j < EMAX; ++j) dl2[i][j] = make_float2(d[j], d[j]);
+        for (int j = 0; j < EMAX; ++j)
+          if (j == lane + 32) v = dl[t][j];
+        dl_out[(size_t)tok * E + lane + 32] = v;
+      }
     }
     for (int c = 0; c < nchunks; ++c) {
       const int h0 = c * hch;
@@ -243,53 +247,50 @@ __global__ void __launch_bounds__(GW * 32, 1)
         stage_wg(ws, wg, h0, hch, H, E);
         __syncthreads();
       }
-      const int nblk = (H - h0 < hch ? H - h0 : hch) >> 6;
-      // software pipeline: dS for steps blk .. blk+PD-1 in flight
-      uint4 buf[PD][TPW];
+      const int hlen = H - h0 < hch ? H - h0 : hch;
+      const int nblk = (hlen + 255) >> 8;
+      auto load = [&](int blk, int t) -> uint4 {
+        const int h = 256 * blk + 8 * lane;
+        return (blk < nblk && h < hlen && kept[t]) ? ld_nc_v4(dS + row[t] + h0 + h)
+                                                   : make_uint4(0, 0, 0, 0);
+      };
+      uint4 nxt[TPW];
 #pragma unroll
-      for (int s = 0; s < PD; ++s)
+      for (int t = 0; t < TPW; ++t) nxt[t] = load(0, t);
+      for (int blk = 0; blk < nblk; ++blk) {
+        float o[TPW][8];
 #pragma unroll
-        for (int i = 0; i < TPW; ++i)
-          buf[s][i] = (kept[i] && s < nblk) ? ld_nc_v4(dS + row[i] + h0 + 64 * s + 8 * l8)
-                                            : make_uint4(0, 0, 0, 0);
-      for (int blk0 = 0; blk0 < nblk; blk0 += PD) {
+        for (int t = 0; t < TPW; ++t) {
+          const float2 f0 = unpack_bf16x2(nxt[t].x), f1 = unpack_bf16x2(nxt[t].y);
+          const float2 f2 = unpack_bf16x2(nxt[t].z), f3 = unpack_bf16x2(nxt[t].w);
+          o[t][0] = f0.x; o[t][1] = f0.y; o[t][2] = f1.x; o[t][3] = f1.y;
+          o[t][4] = f2.x; o[t][5] = f2.y; o[t][6] = f3.x; o[t][7] = f3.y;
+        }
 #pragma unroll
-        for (int s = 0; s < PD; ++s) {
-          const int blk = blk0 + s;
-          if (blk < nblk) {
-            const int h = h0 + 64 * blk + 8 * l8;
-            float2 o[TPW][4];
+        for (int t = 0; t < TPW; ++t) nxt[t] = load(blk + 1, t);
+        const float* wrow = ws + blk * 256 + lane * 4;
 #pragma unroll
-            for (int i = 0; i < TPW; ++i) {
-              o[i][0] = unpack_bf16x2(buf[s][i].x); o[i][1] = unpack_bf16x2(buf[s][i].y);
-              o[i][2] = unpack_bf16x2(buf[s][i].z); o[i][3] = unpack_bf16x2(buf[s][i].w);
-              if (kept[i] && blk + PD < nblk) buf[s][i] = ld_nc_v4(dS + row[i] + h + 64 * PD);
-            }
-            const float* wrow = ws + blk * 64 + l8 * 4;
+        for (int j = 0; j < EMAX; ++j) {
+          const float4 w0 = *reinterpret_cast<const float4*>(wrow + j * hch);
+          const float4 w1 = *reinterpret_cast<const float4*>(wrow + j * hch + 128);
 #pragma unroll
-            for (int j = 0; j < EMAX; ++j) {
-              const float4 w0 = *reinterpret_cast<const float4*>(wrow + j * hch);
-              const float4 w1 = *reinterpret_cast<const float4*>(wrow + j * hch + 32);
-              const float2 p0 = make_float2(w0.x, w0.y), p1 = make_float2(w0.z, w0.w);
-              const float2 p2 = make_float2(w1.x, w1.y), p3 = make_float2(w1.z, w1.w);
+          for (int t = 0; t < TPW; ++t) {
+            const float d = dl[t][j];
+            o[t][0] = fmaf(d, w0.x, o[t][0]); o[t][1] = fmaf(d, w0.y, o[t][1]);
+            o[t][2] = fmaf(d, w0.z, o[t][2]); o[t][3] = fmaf(d, w0.w, o[t][3]);
+            o[t][4] = fmaf(d, w1.x, o[t][4]); o[t][5] = fmaf(d, w1.y, o[t][5]);
+            o[t][6] = fmaf(d, w1.z, o[t][6]); o[t][7] = fmaf(d, w1.w, o[t][7]);
+          }
+        }
+        const int h = h0 + 256 * blk + 8 * lane;
+        if (h - h0 < hlen) {
 #pragma unroll
-              for (int i = 0; i < TPW; ++i) {
-                ffma2(o[i][0], dl2[i][j], p0);
-                ffma2(o[i][1], dl2[i][j], p1);
-                ffma2(o[i][2], dl2[i][j], p2);
-                ffma2(o[i][3], dl2[i][j], p3);
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < TPW; ++i) {
-              if (!valid[i]) continue;
-              const uint4 v = kept[i] ? make_uint4(pack_bf16x2(o[i][0].x, o[i][0].y),
-                                                   pack_bf16x2(o[i][1].x, o[i][1].y),
-                                                   pack_bf16x2(o[i][2].x, o[i][2].y),
-                                                   pack_bf16x2(o[i][3].x, o[i][3].y))
-                                      : make_uint4(0, 0, 0, 0);
-              st_v4(dx + (size_t)(base + 4 * i) * H + h, v);
-            }
+          for (int t = 0; t < TPW; ++t) {
+            if (!valid[t]) continue;
+            const uint4 v = kept[t] ? make_uint4(pack_bf16x2(o[t][0], o[t][1]), pack_bf16x2(o[t][2], o[t][3]),
+                                                 pack_bf16x2(o[t][4], o[t][5]), pack_bf16x2(o[t][6], o[t][7]))
+                                    : make_uint4(0, 0, 0, 0);
+            st_v4(dx + (size_t)(tok0 + t) * H + h, v);
           }
         }
       }
@@ -297,103 +298,113 @@ __global__ void __launch_bounds__(GW * 32, 1)
   }
 }
 
-// dWg = x^T dl: CTA (h block of HB, token split) -> partial[split][h][j]. Thread
-// tile 8 h x JT j; x tile staged as fp32 [TT][half][hq][4] (conflict-free LDS.128),
-// dl staged as (dl, dl) pairs so fma.rn.f32x2 runs over h pairs.
-constexpr int DWG_TT = 16;
+// dWg partials: CTA = (256-wide h block, token split). Warp w handles JW experts
+// (group w % NJG) over token sub-range w / NJG; lane l owns h = hb + 8 l + [0, 8).
+// Per token: one 16-byte x vector and one JW-float dl vector (warp-uniform, L1),
+// JW*8 FMAs as fma.rn.f32x2 over h pairs. Loads run PD tokens ahead. Sub-range
+// partials are combined in shared memory in a fixed order (deterministic).
+constexpr int DWG_WARPS = 8;
 template <int EMAX>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(DWG_WARPS * 32)
     dwg_partial_kernel(const bf16* __restrict__ x, const float* __restrict__ dl, int64_t T, int H,
                        int E, int64_t tok_per_split, float* __restrict__ partial) {
-  constexpr int JT = EMAX < 8 ? EMAX : 8;
-  constexpr int JG = EMAX / JT;
-  constexpr int HQ = (256 / JG) < 64 ? (256 / JG) : 64;  // threads along h
-  constexpr int NT = HQ * JG;                              // threads per CTA
-  constexpr int HB = HQ * 8;                               // h per CTA
-  __shared__ __align__(16) float xs[DWG_TT][HB];
-  __shared__ __align__(16) float2 ds[DWG_TT][EMAX];
-  const int hq = threadIdx.x % HQ, jg = threadIdx.x / HQ;
-  const int hbase = blockIdx.x * HB;
+  constexpr int JW = EMAX <= 32 ? 4 : 8;
+  constexpr int NJG = EMAX / JW > DWG_WARPS ? DWG_WARPS : EMAX / JW;
+  constexpr int TSUB = DWG_WARPS / NJG;
+  constexpr int PD = 4;
+  __shared__ float red[DWG_WARPS][256 * JW];  // per-warp partial tiles (only when TSUB > 1)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jg = warp % NJG, ts = warp / NJG;
+  const int hb = blockIdx.x * 256;
+  const int h = hb + 8 * lane;
+  const bool hok = h < H;
   const int64_t t_begin = (int64_t)blockIdx.y * tok_per_split;
   int64_t t_end = t_begin + tok_per_split;
   if (t_end > T) t_end = T;
-  float2 acc[4][JT];
+  const int64_t span = (t_end - t_begin + TSUB - 1) / TSUB;
+  const int64_t a0 = t_begin + ts * span;
+  int64_t a1 = a0 + span;
+  if (a1 > t_end) a1 = t_end;
+  float2 acc[4][JW];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int j = 0; j < JT; ++j) acc[a][j] = make_float2(0.f, 0.f);
-  // register-staged double buffering: the next tile's x / dl loads are in flight
-  // while the current tile is consumed from shared memory
-  constexpr int XV = (DWG_TT * HQ + NT - 1) / NT;
-  constexpr int DV = (DWG_TT * EMAX + NT - 1) / NT;
-  uint4 xr[XV];
-  float dr[DV];
-  auto load_tile = [&](int64_t tb) {
+    for (int j = 0; j < JW; ++j) acc[k][j] = make_float2(0.f, 0.f);
+  for (int jp = 0; jp < (EMAX / JW + NJG - 1) / NJG; ++jp) {
+    const int j0 = (jg + jp * NJG) * JW;
+    uint4 xb[PD];
+    float db[PD][JW];
+    auto load = [&](int64_t t, int slot_) {
+      const bool ok = t < a1;
+      xb[slot_] = (ok && hok) ? ld_nc_v4(x + (size_t)t * H + h) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int k = 0; k < XV; ++k) {
-      const int i = threadIdx.x + k * NT;
-      const int tt = i / HQ, v = i % HQ;
-      const int64_t t = tb + tt;
-      const int h = hbase + v * 8;
-      xr[k] = (i < DWG_TT * HQ && t < t_end && h < H) ? ld_nc_v4(x + (size_t)t * H + h)
-                                                        : make_uint4(0, 0, 0, 0);
-    }
+      for (int j = 0; j < JW; ++j)
+        db[slot_][j] = (ok && j0 + j < E) ? __ldg(dl + (size_t)t * E + j0 + j) : 0.f;
+    };
 #pragma unroll
-    for (int k = 0; k < DV; ++k) {
-      const int i = threadIdx.x + k * NT;
-      const int tt = i / EMAX, j = i % EMAX;
-      const int64_t t = tb + tt;
-      dr[k] = (i < DWG_TT * EMAX && t < t_end && j < E) ? dl[(size_t)t * E + j] : 0.f;
-    }
-  };
-  if (t_begin < t_end) load_tile(t_begin);
-  for (int64_t tb = t_begin; tb < t_end; tb += DWG_TT) {
-    __syncthreads();
+    for (int s2 = 0; s2 < PD; ++s2) load(a0 + s2, s2);
+    for (int64_t t = a0; t < a1; t += PD) {
 #pragma unroll
-    for (int k = 0; k < XV; ++k) {
-      const int i = threadIdx.x + k * NT;
-      if (i >= DWG_TT * HQ) continue;
-      const int tt = i / HQ, v = i % HQ;
-      const float2 a0 = unpack_bf16x2(xr[k].x), a1 = unpack_bf16x2(xr[k].y),
-                   a2 = unpack_bf16x2(xr[k].z), a3 = unpack_bf16x2(xr[k].w);
-      *reinterpret_cast<float4*>(&xs[tt][v * 4]) = make_float4(a0.x, a0.y, a1.x, a1.y);
-      *reinterpret_cast<float4*>(&xs[tt][HB / 2 + v * 4]) = make_float4(a2.x, a2.y, a3.x, a3.y);
-    }
+      for (int s2 = 0; s2 < PD; ++s2) {
+        if (t + s2 < a1) {
+          const float2 x0 = unpack_bf16x2(xb[s2].x), x1 = unpack_bf16x2(xb[s2].y);
+          const float2 x2 = unpack_bf16x2(xb[s2].z), x3 = unpack_bf16x2(xb[s2].w);
+          float d[JW];
 #pragma unroll
-    for (int k = 0; k < DV; ++k) {
-      const int i = threadIdx.x + k * NT;
-      if (i < DWG_TT * EMAX) ds[i / EMAX][i % EMAX] = make_float2(dr[k], dr[k]);
-    }
-    __syncthreads();
-    if (tb + DWG_TT < t_end) load_tile(tb + DWG_TT);
-#pragma unroll 2
-    for (int tt = 0; tt < DWG_TT; ++tt) {
-      const float4 xa = *reinterpret_cast<const float4*>(&xs[tt][hq * 4]);
-      const float4 xb = *reinterpret_cast<const float4*>(&xs[tt][HB / 2 + hq * 4]);
-      const float2 x0 = make_float2(xa.x, xa.y), x1 = make_float2(xa.z, xa.w);
-      const float2 x2 = make_float2(xb.x, xb.y), x3 = make_float2(xb.z, xb.w);
+          for (int j = 0; j < JW; ++j) d[j] = db[s2][j];
+          load(t + s2 + PD, s2);
 #pragma unroll
-      for (int j = 0; j < JT; ++j) {
-        const float2 d = ds[tt][jg * JT + j];
-        ffma2(acc[0][j], x0, d);
-        ffma2(acc[1][j], x1, d);
-        ffma2(acc[2][j], x2, d);
-        ffma2(acc[3][j], x3, d);
+          for (int j = 0; j < JW; ++j) {
+            const float2 dd = make_float2(d[j], d[j]);
+            ffma2(acc[0][j], x0, dd);
+            ffma2(acc[1][j], x1, dd);
+            ffma2(acc[2][j], x2, dd);
+            ffma2(acc[3][j], x3, dd);
+          }
+        }
       }
     }
-  }
-  const int h = hbase + hq * 8;
-  if (h >= H) return;
+    // combine the TSUB token sub-ranges of this expert group (fixed order) and store
+    if (TSUB > 1) {
+      __syncthreads();
 #pragma unroll
-  for (int j = 0; j < JT; ++j) {
-    const int jj = jg * JT + j;
-    if (jj >= E) continue;
-    float* dst = partial + ((size_t)blockIdx.y * H + h) * E + jj;
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      dst[(size_t)(2 * a) * E] = acc[a][j].x;
-      dst[(size_t)(2 * a + 1) * E] = acc[a][j].y;
+        for (int j = 0; j < JW; ++j) {
+          red[warp][(8 * lane + 2 * k) * JW + j] = acc[k][j].x;
+          red[warp][(8 * lane + 2 * k + 1) * JW + j] = acc[k][j].y;
+        }
+      __syncthreads();
+      if (ts == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int j = 0; j < JW; ++j) {
+            float sx = 0.f, sy = 0.f;
+            for (int u = 0; u < TSUB; ++u) {
+              sx += red[jg + u * NJG][(8 * lane + 2 * k) * JW + j];
+              sy += red[jg + u * NJG][(8 * lane + 2 * k + 1) * JW + j];
+            }
+            acc[k][j] = make_float2(sx, sy);
+          }
+      }
     }
+    if (ts == 0 && hok) {
+#pragma unroll
+      for (int j = 0; j < JW; ++j) {
+        if (j0 + j >= E) continue;
+        float* dst = partial + ((size_t)blockIdx.y * H + h) * E + j0 + j;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          dst[(size_t)(2 * k) * E] = acc[k][j].x;
+          dst[(size_t)(2 * k + 1) * E] = acc[k][j].y;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int j = 0; j < JW; ++j) acc[k][j] = make_float2(0.f, 0.f);
   }
 }
 
@@ -414,7 +425,8 @@ cudaError_t launch_gate_bwd(const void* x, const void* dS, const float* wg, cons
                             const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                             float* dl, float* partial, int nsplit, cudaStream_t s) {
   constexpr int hmax = wg_chunk(EMAX);
-  const int hch = ss.H < hmax ? ss.H : hmax;
+  const int hpad = (ss.H + 255) & ~255;
+  const int hch = hpad < hmax ? hpad : hmax;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_kernel<EMAX, TPW, GW>,
@@ -427,20 +439,17 @@ cudaError_t launch_gate_bwd(const void* x, const void* dS, const float* wg, cons
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t per_cta = (int64_t)GW * 4 * TPW;
+  const int64_t per_cta = (int64_t)GW * TPW;
   int64_t grid = (T + per_cta - 1) / per_cta;
   if (hch >= ss.H && grid > g_sms) grid = g_sms;
   gate_bwd_dx_kernel<EMAX, TPW, GW><<<(unsigned)grid, GW * 32, EMAX * hch * 4, s>>>(
       static_cast<const bf16*>(dS), wg, logits, expert, slot, prob, dp, ss, T, hch,
       static_cast<bf16*>(dx), dl);
   constexpr int EM = EMAX < 4 ? 4 : EMAX;
-  constexpr int JT = EM < 8 ? EM : 8;
-  constexpr int HQ = (256 / (EM / JT)) < 64 ? (256 / (EM / JT)) : 64;
-  constexpr int HB = HQ * 8;
-  const int64_t tps = ((T + nsplit - 1) / nsplit + DWG_TT - 1) / DWG_TT * DWG_TT;
-  dim3 g2((ss.H + HB - 1) / HB, nsplit);
-  dwg_partial_kernel<EM><<<g2, HQ * (EM / JT), 0, s>>>(static_cast<const bf16*>(x), dl, T, ss.H, ss.E, tps,
-                                            partial);
+  const int64_t tps = (T + nsplit - 1) / nsplit;
+  dim3 g2((ss.H + 255) / 256, nsplit);
+  dwg_partial_kernel<EM><<<g2, DWG_WARPS * 32, 0, s>>>(static_cast<const bf16*>(x), dl, T, ss.H,
+                                                       ss.E, tps, partial);
   const int64_t n = (int64_t)ss.H * ss.E;
   dwg_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(partial, nsplit, n, dwg);
   return cudaGetLastError();
@@ -451,9 +460,9 @@ inline unsigned blocks_for(int64_t n) { return (unsigned)((n + WARPS - 1) / WARP
 }  // namespace
 
 int gate_bwd_splits(int64_t T) {
-  int64_t s = T / 128;
+  int64_t s = T / 512;
   if (s < 1) s = 1;
-  if (s > 128) s = 128;
+  if (s > 32) s = 32;
   return (int)s;
 }
 
@@ -496,10 +505,10 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
   if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * ss.H * ss.E, s);
 #define GB(EM, TP, GW) \
   launch_gate_bwd<EM, TP, GW>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, s)
-  if (ss.E <= 4) return GB(4, 2, 16);
-  if (ss.E <= 8) return GB(8, 2, 16);
-  if (ss.E <= 16) return GB(16, 1, 16);
-  if (ss.E <= 32) return GB(32, 1, 16);
+  if (ss.E <= 4) return GB(4, 8, 8);
+  if (ss.E <= 8) return GB(8, 8, 8);
+  if (ss.E <= 16) return GB(16, 4, 8);
+  if (ss.E <= 32) return GB(32, 2, 8);
   return GB(64, 1, 8);
 #undef GB
 }

@@ -1,0 +1,152 @@
+"""Multi-rank MoE-layer parity (launched by tests/test_gpu_multi.py under torchrun).
+
+Every rank builds its shard of a seeded workload (all token groups are generated
+on the host), runs moe_forward/moe_backward through the C ABI with DTD and
+without, and checks against the CPU oracle computed locally for all groups:
+  * routing bit-exact outside logged ties; slots/counts bit-exact after the
+    tie-override protocol;
+  * y, dx, dWg of its token group and dW1/dW2 of its expert shard within
+    relative L2 1e-2 (BASELINE.json);
+  * DTD output == vanilla output bitwise for G_tensor <= 2;
+  * a2a wire bytes: vanilla == G_tensor x DTD, exactly.
+Exit code 0 iff every rank passed.
+
+    torchrun --nproc-per-node N tests/mp_layer_check.py --gt 2 --gep 2 --tokens 512
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import moe_oracle as O  # noqa: E402
+from paper_2305_13525_b200 import MoEConfig, MoELayer, synth  # noqa: E402
+from tests.helpers import REL_L2_BAR, bf16_tensor, rel_l2, tensor_f64  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gt", type=int, default=1)
+    ap.add_argument("--gep", type=int, default=2)
+    ap.add_argument("--tokens", type=int, default=512)
+    ap.add_argument("--hidden", type=int, default=256)
+    ap.add_argument("--ffn", type=int, default=512)
+    ap.add_argument("--experts", type=int, default=8)
+    ap.add_argument("--cf", type=float, default=1.0)
+    a = ap.parse_args()
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    shape = synth.LayerShape("mp", a.tokens, a.hidden, a.ffn, a.experts, a.cf, a.gt, a.gep)
+    assert world % (a.gt * a.gep) == 0
+    gd = world // (a.gt * a.gep)
+    S = world // a.gt  # token groups
+    failures = []
+
+    # host inputs for every token group (groups numbered d*G_ep + ep)
+    xs_b = [synth.make_x(shape, s) for s in range(S)]
+    dys_b = [synth.make_dy(shape, s) for s in range(S)]
+    wg = synth.make_wg(shape)
+    w1_b, w2_b = synth.make_experts(shape)
+
+    results = {}
+    for dtd in (True, False):
+        cfg = MoEConfig.from_shape(shape, dtd=dtd)
+        layer = MoELayer(cfg, world, rank, dev)
+        L = layer.layout
+        s = L["d"] * a.gep + L["ep"]
+        w1s, w2s = synth.shard_experts(w1_b, w2_b, shape, L["ep"], L["t"])
+        x = bf16_tensor(xs_b[s])
+        dy = bf16_tensor(dys_b[s])
+        wgt = torch.from_numpy(wg).to(dev)
+        w1 = bf16_tensor(w1s)
+        w2 = bf16_tensor(w2s)
+        y, saved = layer.moe_forward(x, wgt, w1, w2)
+        dx, dwg, dw1, dw2 = layer.moe_backward(dy, saved, x, wgt, w1, w2)
+        rt = layer.moe_routing(saved)
+        torch.cuda.synchronize()
+        st = layer.moe_stats()
+        results[dtd] = {"y": y.clone(), "dx": dx.clone(), "dwg": dwg.clone(), "dw1": dw1.clone(),
+                        "dw2": dw2.clone(), "rt": {k: v.cpu().numpy() for k, v in rt.items()},
+                        "stats": st, "layout": L, "group": s}
+        layer.close()
+
+    L = results[True]["layout"]
+    s = results[True]["group"]
+    # ---- oracle over the EP group of this rank (G_data replicas are independent)
+    d = L["d"]
+    groups = [d * a.gep + ep for ep in range(a.gep)]
+    xs = [O.decode_bf16(xs_b[g]) for g in groups]
+    dys = [O.decode_bf16(dys_b[g]) for g in groups]
+    w1d, w2d = O.decode_bf16(w1_b), O.decode_bf16(w2_b)
+    wgd = wg.astype(np.float64)
+    cap = O.capacity(a.tokens, a.experts, a.cf, a.gt)
+    # tie protocol needs every group's GPU routing: gather expert/gap from the t == 0 ranks
+    ge = torch.from_numpy(results[True]["rt"]["expert"]).to(dev)
+    gg = torch.from_numpy(results[True]["rt"]["gap"]).to(dev)
+    all_e = [torch.empty_like(ge) for _ in range(world)]
+    all_g = [torch.empty_like(gg) for _ in range(world)]
+    dist.all_gather(all_e, ge)
+    dist.all_gather(all_g, gg)
+    overrides = []
+    for gi, g in enumerate(groups):
+        r_rank = g * a.gt  # rank (d, ep, t=0) of group g
+        ex = all_e[r_rank].cpu().numpy()
+        gp = all_g[r_rank].cpu().numpy()
+        r0 = O.route(xs[gi], wgd, cap)
+        tie = (r0.gap < O.TIE_GAP) | (gp < O.TIE_GAP)
+        bad = np.nonzero((ex != r0.expert) & ~tie)[0]
+        if bad.size:
+            failures.append(f"group {g}: routing mismatch outside ties at {bad[:8]}")
+        overrides.append((np.nonzero(tie)[0], ex[tie]))
+    ref = O.layer(xs, dys, wgd, w1d, w2d, a.cf, a.gt, overrides=overrides)
+    gi = groups.index(s)
+    r = ref["routing"][gi]
+    g = results[True]
+    if not (g["rt"]["slot"] == r.slot).all():
+        failures.append("slot mismatch")
+    if not (g["rt"]["count"] == r.count).all():
+        failures.append("count mismatch")
+    El, Fl = L["experts_local"], L["ffn_local"]
+    es = slice(L["ep"] * El, (L["ep"] + 1) * El)
+    fs = slice(L["t"] * Fl, (L["t"] + 1) * Fl)
+    errs = {"y": rel_l2(tensor_f64(g["y"]), ref["y"][gi]),
+            "dx": rel_l2(tensor_f64(g["dx"]), ref["dx"][gi]),
+            "dwg": rel_l2(g["dwg"].cpu().numpy(), ref["dwg"][gi]),
+            "dw1": rel_l2(tensor_f64(g["dw1"]), ref["dw1"][es, fs, :]),
+            "dw2": rel_l2(tensor_f64(g["dw2"]), ref["dw2"][es, :, fs])}
+    for k, v in errs.items():
+        if not v <= REL_L2_BAR:
+            failures.append(f"{k} rel L2 {v:.3e}")
+    # ---- DTD vs vanilla
+    v, t_ = results[False], results[True]
+    for k in ("y", "dx", "dwg", "dw1", "dw2"):
+        same = torch.equal(v[k], t_[k])
+        if a.gt <= 2 and not same:
+            failures.append(f"DTD != vanilla (bitwise) for {k}")
+        if not same and rel_l2(tensor_f64(v[k]), tensor_f64(t_[k])) > 1e-2:
+            failures.append(f"DTD vs vanilla differ for {k}")
+    a2a_dtd = t_["stats"]["wire_bytes"]["a2a"]
+    a2a_van = v["stats"]["wire_bytes"]["a2a"]
+    if a2a_dtd * a.gt != a2a_van:
+        failures.append(f"a2a bytes: dtd {a2a_dtd} x {a.gt} != vanilla {a2a_van}")
+    print(f"[rank {rank}] (d,ep,t)=({L['d']},{L['ep']},{L['t']}) errs="
+          + " ".join(f"{k}={e:.2e}" for k, e in errs.items())
+          + f" a2a dtd={a2a_dtd} van={a2a_van} calls={t_['stats']['calls']}"
+          + (" FAIL: " + "; ".join(failures) if failures else " ok"), flush=True)
+    flag = torch.tensor([len(failures)], device=dev)
+    dist.all_reduce(flag)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
