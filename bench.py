@@ -38,8 +38,8 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=None, choices=[None, "1.3b", "2.7b", "6.7b"])
     p.add_argument("--vanilla", action="store_true", help="disable DTD (G_tensor > 1 configs)")
@@ -279,13 +279,26 @@ def main():
     gemm_ms = st["kernel_ms"]["gemm"] / args.steps
     peaks, peak_src = load_peaks()
     achieved = gemm_flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
-    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    # clocks at max during the timed region -> compare with the burst peak (conservative);
+    # power-capped clocks -> the sustained peak (MEASURED_PEAKS.json, B200_PROFILING.md)
+    capped = bool(clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] < 0.97 * clk["sm_max_mhz"])
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) if capped else peaks["bf16_tflops"]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("workload") == name:
+            traffic = tj["dram_bytes_per_launch"]
+    except Exception:
+        pass
     launches_per_step = sum(st["kernel_launches"].values()) / args.steps
     gemm_launch_ms = gemm_ms / 6.0
-    roofline = {"bound": "tensor", "kernel": "gemm_kernel (tcgen05, 6 launches/step)",
+    roofline = {"bound": "tensor", "kernel": "gemm2_kernel (tcgen05 cta_group::2, 6 launches/step)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "peak_kind": f"{peak_src} bf16 sustained (kernel inside a long step)",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_kind": f"{peak_src} bf16 {'sustained' if capped else 'burst'}",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "frac_of_sustained": (achieved / peaks.get('bf16_tflops_sustained', peak)) if achieved else None,
+                "algorithmic_flop_per_launch": gemm_flops_step / 6.0,
                 "ms_per_launch": gemm_launch_ms, "share_of_step": gemm_ms / ms}
     per_class = {k: v / args.steps for k, v in st["kernel_ms"].items()}
 
