@@ -167,11 +167,21 @@ def run_cpu_baseline(H, F, E, sample_tokens=256, budget_s=20.0):
 
 
 def reference_arm(args, world, rank):
+    """The oracle, as it stands, on this host's cores (the only reference this
+    tier has: /root/reference holds a paper, not code). Each step is a bounded
+    token sample of the same workload, sized so W + K steps take ~2 minutes."""
     if rank != 0:
         return
     name, T, H, F, E, gt, gep = workload(args, 1)
-    sample = 256
-    state = oracle_state(H, F, E, sample)
+    probe = 64
+    state = oracle_state(H, F, E, probe)
+    t64 = cpu_oracle_step(None, probe, state)
+    t64 = min(t64, cpu_oracle_step(None, probe, state))
+    n = max(args.steps + args.warmup, 1)
+    sample = int(max(16, min(256, probe * 120.0 / (n * max(t64, 1e-3)))))
+    sample -= sample % 16
+    if sample != probe:
+        state = oracle_state(H, F, E, sample)
     for _ in range(args.warmup):
         cpu_oracle_step(None, sample, state)
     t0 = time.perf_counter()
