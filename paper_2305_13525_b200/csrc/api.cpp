@@ -511,9 +511,10 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   }
   // B10 dispatch-bwd + gate-bwd
   {
-    Scope sc_(c, MOE_K_GATE_BWD, st, 3);
+    Scope sc_(c, MOE_K_GATE_BWD, st, 4);
     CUDA_TRY(c, gate_bwd(x, dS, wg, logits, expert, slot, prob, dp, ss, d.T, dx, dwg,
-                         at<float>(c->scratch, sc.dl), at<float>(c->scratch, sc.dwgp), sc.nsplit, st));
+                         at<float>(c->scratch, sc.dl), at<float>(c->scratch, sc.dwgp), sc.nsplit,
+                         at<uint8_t>(c->scratch, sc.wpk), st));
   }
   c->last_stream = st;
   return MOE_OK;

@@ -1,0 +1,404 @@
+// gate_bwd.cu — B10 on tensor cores (legacy warp MMA; the contractions are tiny):
+//   dl_tj = dp_t p_t (delta_{j e*} - softmax(l_t)_j)          (kept tokens; 0 if dropped)
+//   dx_t  = dS[row(t)] + sum_j dl_tj Wg[:, j]                   (0 if dropped)
+//   dWg   = sum_t x_t^T dl_t                                     (deterministic split-K)
+// dl and Wg are fp32; each is split into bf16 hi + lo so the products carry ~16
+// mantissa bits (relative error ~2^-17 per term, far inside the 1e-2 gradient
+// tolerance); x is exact bf16. Routing-critical arithmetic (the forward gate) stays
+// on fp32 CUDA cores in route.cu.
+#include "common.cuh"
+#include "internal.h"
+
+namespace moe {
+namespace {
+
+__device__ __forceinline__ size_t slot_row2(const SlotSpace& ss, int e, int64_t c) {
+  const int64_t tt = c / ss.Cs, cs = c - tt * ss.Cs;
+  return ((size_t)(tt * ss.E + e) * ss.Cs + cs) * ss.H;
+}
+
+// ------------------------------------------------------------------ Wg -> B' fragments
+// B'[k][h] for k in [0, 3*EPK): block 0 = hi(Wg), 1 = hi(Wg), 2 = lo(Wg) (paired with
+// A' = [hi(dl) | lo(dl) | hi(dl)]). Packed per (n-tile, k-step) in m16n8k16 B-fragment
+// order: word (nt*KS + ks)*64 + lane*2 + {0,1} = {b0, b1} of lane.
+__global__ void wg_pack_kernel(const float* __restrict__ wg, int H, int E, int EPK,
+                               uint32_t* __restrict__ packed) {
+  const int KS = 3 * EPK / 16;
+  const int ntiles = H / 8;
+  const int64_t n = (int64_t)ntiles * KS * 32;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int lane = (int)(i & 31);
+  const int ks = (int)((i >> 5) % KS);
+  const int nt = (int)((i >> 5) / KS);
+  const int g = lane >> 2, tig = lane & 3;
+  const int h = nt * 8 + g;
+  auto val = [&](int k) -> bf16 {
+    const int blk = k / EPK, j = k % EPK;
+    const float v = (j < E) ? wg[(size_t)h * E + j] : 0.f;
+    bf16 hi, lo;
+    split_bf16(v, hi, lo);
+    return blk == 2 ? lo : hi;
+  };
+  const int k0 = 16 * ks + 2 * tig;
+  packed[i * 2] = pack2(val(k0), val(k0 + 1));
+  packed[i * 2 + 1] = pack2(val(k0 + 8), val(k0 + 9));
+}
+
+// ------------------------------------------------------------------ dx (+ dl)
+// CTA = 4 warps; warp w owns one m-tile of 16 tokens. It builds the A' fragments
+// of its tokens (softmax recomputed from the saved logits; lane 4g+tig covers
+// tokens g, g+8 and experts 16kk + 2tig + {0,1,8,9}), writes dl [T][E] fp32 for
+// dWg, then walks H in 64-wide chunks: 8 n-tiles x KS MMAs, the fp32 results are
+// staged in a per-warp shared tile [16][64] and re-read as 16-byte row pieces so
+// dS[row(t)] is added and dx stored with coalesced 16-byte accesses.
+constexpr int DX_WARPS = 4;
+template <int EPK>
+__global__ void __launch_bounds__(DX_WARPS * 32)
+    gate_bwd_dx_mma_kernel(const bf16* __restrict__ dS, const uint32_t* __restrict__ wpk,
+                           const float* __restrict__ logits, const int32_t* __restrict__ expert,
+                           const int32_t* __restrict__ slot, const float* __restrict__ prob,
+                           const float* __restrict__ dp, SlotSpace ss, int64_t T,
+                           bf16* __restrict__ dx, float* __restrict__ dl_out) {
+  constexpr int KK = EPK / 16;  // k-steps per block of A'
+  constexpr int KS = 3 * KK;
+  __shared__ __align__(16) float stage[DX_WARPS][16][64 + 4];
+  extern __shared__ __align__(16) uint32_t wsm[];  // this CTA's B' fragments
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int E = ss.E, H = ss.H;
+  const int64_t t0 = ((int64_t)blockIdx.x * DX_WARPS + warp) * 16;
+  // H is split over gridDim.y CTAs (more warps in flight for this HBM-bound pass)
+  const int ntiles_all = H / 8;
+  const int per = ((ntiles_all + gridDim.y - 1) / gridDim.y + 7) & ~7;
+  const int nt_begin = blockIdx.y * per;
+  const int nt_end = nt_begin + per < ntiles_all ? nt_begin + per : ntiles_all;
+  {
+    const int nwords = (nt_end - nt_begin) * KS * 64;
+    const uint4* src = reinterpret_cast<const uint4*>(wpk + (size_t)nt_begin * KS * 64);
+    for (int i = threadIdx.x; i < nwords / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(wsm)[i] = __ldg(src + i);
+  }
+  __syncthreads();
+
+  uint32_t afr[KS][4];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int64_t t = t0 + g + 8 * half;
+    const int s = t < T ? slot[t] : -1;
+    float dlv[KK][4];  // j = 16 kk + 2 tig + {0, 1, 8, 9}
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dlv[kk][q] = 0.f;
+    if (s >= 0) {
+      const int e = expert[t];
+      const float* lg = logits + (size_t)t * E;
+      float m = -3.402823e38f;
+      for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
+      float den = 0.f;
+      for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
+      const float gsc = dp[t] * prob[t];
+      const float inv = 1.f / den;
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
+          if (j < E) dlv[kk][q] = gsc * ((j == e ? 1.f : 0.f) - expf(lg[j] - m) * inv);
+        }
+    }
+    if (t < T && blockIdx.y == 0) {
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
+          if (j < E) dl_out[(size_t)t * E + j] = dlv[kk][q];
+        }
+    }
+    // A' fragments: a0/a2 rows g (half 0), a1/a3 rows g+8 (half 1)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int blk = ks / KK, kk = ks % KK;
+      bf16 h0, l0, h1, l1, h2, l2, h3, l3;
+      split_bf16(dlv[kk][0], h0, l0);
+      split_bf16(dlv[kk][1], h1, l1);
+      split_bf16(dlv[kk][2], h2, l2);
+      split_bf16(dlv[kk][3], h3, l3);
+      afr[ks][half] = blk == 1 ? pack2(l0, l1) : pack2(h0, h1);      // cols 2tig, 2tig+1
+      afr[ks][2 + half] = blk == 1 ? pack2(l2, l3) : pack2(h2, h3);  // cols 2tig+8, 2tig+9
+    }
+  }
+  // per-lane row pieces for the coalesced pass: piece p = lane + 32 k (k < 4) of the
+  // 16 x 64 tile -> row p / 8, 8 columns at 8 * (p % 8)
+  size_t rowoff[4];
+  bool kept[4], valid[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = (lane + 32 * k) >> 3;
+    const int64_t t = t0 + r;
+    valid[k] = t < T;
+    const int s = valid[k] ? slot[t] : -1;
+    kept[k] = s >= 0;
+    rowoff[k] = kept[k] ? slot_row2(ss, expert[t], s) : 0;
+  }
+
+  const int ntiles = nt_end;
+  auto load_ds = [&](int n0, uint4 (&dsv)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 8 * ((lane + 32 * k) & 7);
+      const int h = 8 * n0 + c;
+      dsv[k] = (kept[k] && n0 < ntiles && h < 8 * ntiles) ? ld_nc_v4(dS + rowoff[k] + h)
+                                                           : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 dsn[4];
+  load_ds(nt_begin, dsn);
+  for (int n0 = nt_begin; n0 < ntiles; n0 += 8) {
+    uint4 dsv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dsv[k] = dsn[k];
+    load_ds(n0 + 8, dsn);  // next chunk's dS in flight during this chunk's MMAs
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int nt = n0 + j;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (nt < ntiles) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint2 v = *reinterpret_cast<const uint2*>(wsm + ((nt - nt_begin) * KS + ks) * 64 + lane * 2);
+          mma_bf16_16816(acc, afr[ks], v.x, v.y);
+        }
+      }
+      stage[warp][g][8 * j + 2 * tig] = acc[0];
+      stage[warp][g][8 * j + 2 * tig + 1] = acc[1];
+      stage[warp][g + 8][8 * j + 2 * tig] = acc[2];
+      stage[warp][g + 8][8 * j + 2 * tig + 1] = acc[3];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int p = lane + 32 * k, r = p >> 3, c = 8 * (p & 7);
+      const int h = 8 * n0 + c;
+      if (!valid[k] || h >= 8 * ntiles) continue;
+      const float4 g0 = *reinterpret_cast<const float4*>(&stage[warp][r][c]);
+      const float4 g1 = *reinterpret_cast<const float4*>(&stage[warp][r][c + 4]);
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (kept[k]) {
+        const float2 s0 = unpack_bf16x2(dsv[k].x), s1 = unpack_bf16x2(dsv[k].y);
+        const float2 s2 = unpack_bf16x2(dsv[k].z), s3 = unpack_bf16x2(dsv[k].w);
+        o = make_uint4(pack_bf16x2(s0.x + g0.x, s0.y + g0.y), pack_bf16x2(s1.x + g0.z, s1.y + g0.w),
+                       pack_bf16x2(s2.x + g1.x, s2.y + g1.y), pack_bf16x2(s3.x + g1.z, s3.y + g1.w));
+      }
+      st_v4(dx + (size_t)(t0 + r) * H + h, o);
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ dWg partials
+// D[e'][h] = sum_t A[e'][t] B[t][h], A = [hi(dl) | lo(dl)]^T (2*EP rows), B = x.
+// CTA = 8 warps over HB = 8*NT*8 columns of h, one token split; tiles of 32 tokens
+// staged in shared memory (register-prefetched one tile ahead), fragments via
+// ldmatrix.trans. dWg[h][e] = D[e][h] + D[EP+e][h] is written as a partial.
+constexpr int DW_TT = 32;
+template <int EP>
+__global__ void __launch_bounds__(256)
+    dwg_mma_kernel(const bf16* __restrict__ x, const float* __restrict__ dl, int64_t T, int H, int E,
+                   int64_t tok_per_split, float* __restrict__ partial) {
+  constexpr int M2 = 2 * EP;            // rows of A (hi | lo)
+  constexpr int MT = (M2 + 15) / 16;    // m-tiles
+  constexpr int MROWS = MT * 16;
+  constexpr int NT = EP <= 32 ? 4 : 2;  // n-tiles per warp
+  constexpr int HB = 8 * NT * 8;        // h per CTA
+  constexpr int SA = MROWS + 8;         // dl_s row stride (bf16 elements), +16 B pad
+  constexpr int SB = HB + 8;            // x_s row stride
+  __shared__ __align__(16) bf16 dl_s[DW_TT][SA];
+  __shared__ __align__(16) bf16 x_s[DW_TT][SB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hb = blockIdx.x * HB;
+  const int64_t t_begin = (int64_t)blockIdx.y * tok_per_split;
+  int64_t t_end = t_begin + tok_per_split;
+  if (t_end > T) t_end = T;
+
+  constexpr int XV = DW_TT * HB / 8 / 256;  // 16-byte x vectors per thread per tile
+  constexpr int DV = (DW_TT * EP + 255) / 256;
+  uint4 xr[XV];
+  float dr[DV];
+  auto load_tile = [&](int64_t tb) {
+#pragma unroll
+    for (int k = 0; k < XV; ++k) {
+      const int i = threadIdx.x + k * 256;
+      const int tt = i / (HB / 8), v = i % (HB / 8);
+      const int64_t t = tb + tt;
+      const int h = hb + 8 * v;
+      xr[k] = (t < t_end && h < H) ? ld_nc_v4(x + (size_t)t * H + h) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < DV; ++k) {
+      const int i = threadIdx.x + k * 256;
+      const int tt = i / EP, j = i % EP;
+      const int64_t t = tb + tt;
+      dr[k] = (i < DW_TT * EP && t < t_end && j < E) ? __ldg(dl + (size_t)t * E + j) : 0.f;
+    }
+  };
+  float acc[MT][NT][4];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.f;
+  // rows MROWS > 2*EP (only when EP == 4) stay zero
+  for (int i = threadIdx.x; i < DW_TT * SA; i += 256) (&dl_s[0][0])[i] = __float2bfloat16_rn(0.f);
+  if (t_begin < t_end) load_tile(t_begin);
+  for (int64_t tb = t_begin; tb < t_end; tb += DW_TT) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < XV; ++k) {
+      const int i = threadIdx.x + k * 256;
+      const int tt = i / (HB / 8), v = i % (HB / 8);
+      *reinterpret_cast<uint4*>(&x_s[tt][8 * v]) = xr[k];
+    }
+#pragma unroll
+    for (int k = 0; k < DV; ++k) {
+      const int i = threadIdx.x + k * 256;
+      if (i < DW_TT * EP) {
+        const int tt = i / EP, j = i % EP;
+        bf16 hi, lo;
+        split_bf16(dr[k], hi, lo);
+        dl_s[tt][j] = hi;
+        dl_s[tt][EP + j] = lo;
+      }
+    }
+    __syncthreads();
+    if (tb + DW_TT < t_end) load_tile(tb + DW_TT);
+#pragma unroll
+    for (int ks = 0; ks < DW_TT / 16; ++ks) {
+      const int mi = lane >> 3, r = lane & 7;
+      uint32_t afr[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int t = 16 * ks + r + 8 * (mi >> 1);
+        const int e = 16 * mt + 8 * (mi & 1);
+        ldmatrix_x4_trans(afr[mt], smem_u32(&dl_s[t][e]));
+      }
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        const int t = 16 * ks + r + 8 * (mi & 1);
+        const int hcol = warp * NT * 8 + 16 * np + 8 * (mi >> 1);
+        uint32_t bfr[4];
+        ldmatrix_x4_trans(bfr, smem_u32(&x_s[t][hcol]));
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          mma_bf16_16816(acc[mt][2 * np], afr[mt], bfr[0], bfr[1]);
+          mma_bf16_16816(acc[mt][2 * np + 1], afr[mt], bfr[2], bfr[3]);
+        }
+      }
+    }
+  }
+  // epilogue: rows e' = 16 mt + g (+8); cols h = hb + warp*NT*8 + 8 nt + 2 tig (+1)
+  const int g = lane >> 2, tig = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int er = 16 * mt + g + 8 * half;  // row of D
+      if (er >= EP) continue;                 // lo rows are folded into their hi row
+      const int elo = er + EP;
+      const int mlo = elo / 16, hlo = (elo % 16) >= 8 ? 1 : 0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int h = hb + warp * NT * 8 + 8 * nt + 2 * tig;
+        if (er >= E || h >= H) continue;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float v = acc[mt][nt][2 * half + c];
+#pragma unroll
+          for (int m2 = 0; m2 < MT; ++m2)
+            if (m2 == mlo) v += hlo ? acc[m2][nt][2 + c] : acc[m2][nt][c];
+          partial[((size_t)blockIdx.y * H + h + c) * E + er] = v;
+        }
+      }
+    }
+}
+
+__global__ void dwg_reduce2_kernel(const float* __restrict__ partial, int nsplit, int64_t n,
+                                   float* __restrict__ dwg) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int k = 0; k < nsplit; ++k) s += partial[(size_t)k * n + i];
+  dwg[i] = s;
+}
+
+template <int EPK, int EP>
+cudaError_t run(const void* x, const void* dS, const float* wg, const float* logits,
+                const int32_t* expert, const int32_t* slot, const float* prob, const float* dp,
+                const SlotSpace& ss, int64_t T, void* dx, float* dwg, float* dl, float* partial,
+                int nsplit, uint32_t* wpk, cudaStream_t s) {
+  const int H = ss.H, E = ss.E;
+  const int KS = 3 * EPK / 16;
+  const int64_t npack = (int64_t)(H / 8) * KS * 32;
+  wg_pack_kernel<<<(unsigned)((npack + 255) / 256), 256, 0, s>>>(wg, H, E, EPK, wpk);
+  const int64_t tb = 16 * DX_WARPS;
+  // split H so that (a) enough warps are in flight and (b) the CTA's B' slice
+  // (per * KS * 256 bytes) fits in 96 KiB of shared memory
+  const int ntiles = H / 8;
+  int hsplit = H >= 1024 ? 4 : 1;
+  auto slice_bytes = [&](int hs) { return (size_t)(((ntiles + hs - 1) / hs + 7) & ~7) * KS * 256; };
+  while (slice_bytes(hsplit) > 96 * 1024) hsplit *= 2;
+  const size_t smem = slice_bytes(hsplit);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_mma_kernel<EPK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  gate_bwd_dx_mma_kernel<EPK><<<dim3((unsigned)((T + tb - 1) / tb), hsplit), DX_WARPS * 32, smem, s>>>(
+      static_cast<const bf16*>(dS), wpk, logits, expert, slot, prob, dp, ss, T,
+      static_cast<bf16*>(dx), dl);
+  constexpr int NT = EP <= 32 ? 4 : 2;
+  constexpr int HB = 8 * NT * 8;
+  const int64_t tps = ((T + nsplit - 1) / nsplit + DW_TT - 1) / DW_TT * DW_TT;
+  dim3 g2((H + HB - 1) / HB, nsplit);
+  dwg_mma_kernel<EP><<<g2, 256, 0, s>>>(static_cast<const bf16*>(x), dl, T, H, E, tps, partial);
+  const int64_t n = (int64_t)H * E;
+  dwg_reduce2_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(partial, nsplit, n, dwg);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t gate_bwd_pack_bytes(int H, int E) {
+  const int EPK = E <= 16 ? 16 : (E <= 32 ? 32 : 64);
+  return (size_t)(H / 8) * (3 * EPK / 16) * 64 * 4;
+}
+
+cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float* logits,
+                     const int32_t* expert, const int32_t* slot, const float* prob,
+                     const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
+                     float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
+                     cudaStream_t s) {
+  if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * ss.H * ss.E, s);
+  uint32_t* wpk = static_cast<uint32_t*>(pack_scratch);
+#define RUN(EPK, EP) \
+  run<EPK, EP>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, wpk, s)
+  if (ss.E <= 8) return RUN(16, 8);  // EP >= 8: a lo row sits in the same thread as its hi row
+  if (ss.E <= 16) return RUN(16, 16);
+  if (ss.E <= 32) return RUN(32, 32);
+  return RUN(64, 64);
+#undef RUN
+}
+
+int gate_bwd_splits(int64_t T) {
+  int64_t s = T / 512;
+  if (s < 1) s = 1;
+  if (s > 32) s = 32;
+  return (int)s;
+}
+
+}  // namespace moe

@@ -101,6 +101,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dp = b.take((size_t)d.T * 4);
   sc->dl = b.take((size_t)d.T * d.E * 4);
   sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
+  sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));
   sc->dY = b.take(expert_space);
   sc->dO = solo ? sc->dY : b.take(slot_space);
   sc->dH = b.take(ffn_space);

@@ -34,7 +34,7 @@ struct ScratchLayout {
   // forward
   size_t local_rank, block_hist, D, Ypart;
   // backward
-  size_t dp, dl, dwgp, dO, dY, dH, dXp, dS;
+  size_t dp, dl, dwgp, wpk, dO, dY, dH, dXp, dS;
   size_t total;
   bool D_in_saved, Y_in_saved;  // world == 1: D aliases saved.X, Ypart aliases saved.O
   bool dO_is_dY, dXp_is_dS;     // world == 1: slot space == expert space

@@ -22,97 +22,151 @@ namespace moe {
 namespace {
 
 
-// One warp owns TPW tokens at a time; lane l covers h = 256 i + 8 l + [0, 8)
-// (one coalesced 16-byte x vector per token per step). Wg comes from shared
-// memory (resident when it fits in 128 KiB, else streamed per H-chunk), and
-// every Wg value a lane loads is reused for its TPW tokens from registers.
-// Each lane sums H/32 terms, then a fixed butterfly over the 32 lanes.
+// Wg staged as expert pairs: wp[ep][blk][kp][lane][4] holds, for h = 256 blk + 8 lane
+// + 2 kp + {0,1} and e = 2 ep + {0,1}: (w[h][e0], w[h][e1], w[h+1][e0], w[h+1][e1]).
+// One LDS.128 per (ep, blk, kp) across the warp reads 512 contiguous bytes.
+__device__ __forceinline__ int wp_index(int e, int hl, int hch) {
+  const int blk = hl >> 8, r = hl & 255, ln = r >> 3, k = r & 7;
+  return (e >> 1) * (2 * hch) + blk * 512 + (k >> 1) * 128 + ln * 4 + (k & 1) * 2 + (e & 1);
+}
+
+__device__ __forceinline__ void stage_wg_pairs(float* ws, const float* __restrict__ wg, int h0,
+                                               int hch, int H, int E, int emax) {
+  constexpr int U = 16;
+  const int n = hch * emax;
+  const int nt = blockDim.x;
+  for (int b = threadIdx.x; b < n; b += U * nt) {
+    float v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = b + k * nt;
+      const int hl = i / emax, e = i - hl * emax;
+      v[k] = (i < n && e < E && h0 + hl < H) ? __ldg(wg + (size_t)(h0 + hl) * E + e) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = b + k * nt;
+      if (i < n) {
+        const int hl = i / emax, e = i - hl * emax;
+        ws[wp_index(e, hl, hch)] = v[k];
+      }
+    }
+  }
+}
+
+// One warp owns TPW tokens at a time; lane l covers h = 256 i + 8 l + [0, 8).
+// x streams through a per-warp double buffer in shared memory (cp.async, one
+// coalesced 16-byte piece per lane per token per 256-wide step); Wg comes from
+// shared memory (resident when it fits in 128 KiB, else streamed per H-chunk);
+// every Wg pair a lane loads is reused for its TPW tokens, and the FMAs are packed
+// fma.rn.f32x2 over expert pairs: (acc_e0, acc_e1) += (x, x) * (w_e0, w_e1).
+// Each lane sums H/32 terms per expert in h order, then a fixed butterfly.
 template <int EMAX, int TPW, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     gate_kernel(const bf16* __restrict__ x, const float* __restrict__ wg,
                 const int32_t* __restrict__ forced, int64_t T, int H, int E, int hch,
                 float* __restrict__ logits, int32_t* __restrict__ expert,
                 float* __restrict__ prob, float* __restrict__ gap, int32_t* __restrict__ ties) {
-  extern __shared__ __align__(16) float ws[];  // [EMAX][hch], see ws_index
+  constexpr int EP = EMAX / 2;
+  extern __shared__ __align__(16) float ws[];  // [EP][2*hch] (see wp_index), then x buffers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // x double buffer of this warp: [2][TPW][256] bf16
+  bf16* xs = reinterpret_cast<bf16*>(ws + EMAX * hch) + (size_t)warp * 2 * TPW * 256;
   constexpr int PER_CTA = WARPS * TPW;
   const int nchunks = (H + hch - 1) / hch;
   const bool resident = nchunks == 1;
   if (resident) {
-    stage_wg(ws, wg, 0, hch, H, E);
+    stage_wg_pairs(ws, wg, 0, hch, H, E, EMAX);
     __syncthreads();
   }
   const int64_t nbatch = (T + PER_CTA - 1) / PER_CTA;
   for (int64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
     const int64_t tok0 = b * PER_CTA + warp * TPW;
-    float acc[TPW][EMAX];
+    float2 acc[TPW][EP];
 #pragma unroll
     for (int t = 0; t < TPW; ++t)
 #pragma unroll
-      for (int e = 0; e < EMAX; ++e) acc[t][e] = 0.f;
+      for (int e = 0; e < EP; ++e) acc[t][e] = make_float2(0.f, 0.f);
 
     for (int c = 0; c < nchunks; ++c) {
       const int h0 = c * hch;
       if (!resident) {
         __syncthreads();
-        stage_wg(ws, wg, h0, hch, H, E);
+        stage_wg_pairs(ws, wg, h0, hch, H, E, EMAX);
         __syncthreads();
       }
       const int hlen = H - h0 < hch ? H - h0 : hch;
       const int nblk = (hlen + 255) >> 8;
-      auto load = [&](int blk, int t) -> uint4 {
-        const int h = 256 * blk + 8 * lane;
-        const int64_t tok = tok0 + t;
-        return (blk < nblk && h < hlen && tok < T) ? ld_nc_v4(x + (size_t)tok * H + h0 + h)
-                                                   : make_uint4(0, 0, 0, 0);
-      };
-      uint4 nxt[TPW];
-#pragma unroll
-      for (int t = 0; t < TPW; ++t) nxt[t] = load(0, t);
-      for (int blk = 0; blk < nblk; ++blk) {
-        float xv[TPW][8];
+      auto issue = [&](int blk) {
+        bf16* dst = xs + (blk & 1) * TPW * 256;
 #pragma unroll
         for (int t = 0; t < TPW; ++t) {
-          const float2 f0 = unpack_bf16x2(nxt[t].x), f1 = unpack_bf16x2(nxt[t].y);
-          const float2 f2 = unpack_bf16x2(nxt[t].z), f3 = unpack_bf16x2(nxt[t].w);
-          xv[t][0] = f0.x; xv[t][1] = f0.y; xv[t][2] = f1.x; xv[t][3] = f1.y;
-          xv[t][4] = f2.x; xv[t][5] = f2.y; xv[t][6] = f3.x; xv[t][7] = f3.y;
+          const int h = 256 * blk + 8 * lane;
+          const int64_t tok = tok0 + t;
+          const bool ok = blk < nblk && h < hlen && tok < T;
+          cp_async_16(smem_u32(dst + t * 256 + 8 * lane), ok ? x + (size_t)tok * H + h0 + h : x, ok);
         }
+        cp_async_commit();
+      };
+      issue(0);
+      for (int blk = 0; blk < nblk; ++blk) {
+        issue(blk + 1);
+        cp_async_wait_1();  // this lane's pieces of step blk have landed
+        const bf16* cur = xs + (blk & 1) * TPW * 256;
+        uint4 xv[TPW];
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) nxt[t] = load(blk + 1, t);
-        const float* wrow = ws + blk * 256 + lane * 4;
+        for (int t = 0; t < TPW; ++t)
+          xv[t] = *reinterpret_cast<const uint4*>(cur + t * 256 + 8 * lane);
+        const float* wrow = ws + blk * 512 + lane * 4;
 #pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          const float4 w0 = *reinterpret_cast<const float4*>(wrow + e * hch);
-          const float4 w1 = *reinterpret_cast<const float4*>(wrow + e * hch + 128);
+        for (int kp = 0; kp < 4; ++kp) {
+          float2 xd0[TPW], xd1[TPW];  // (x, x) for h = 2 kp and 2 kp + 1
 #pragma unroll
           for (int t = 0; t < TPW; ++t) {
-            float a = acc[t][e];
-            a = fmaf(xv[t][0], w0.x, a); a = fmaf(xv[t][1], w0.y, a);
-            a = fmaf(xv[t][2], w0.z, a); a = fmaf(xv[t][3], w0.w, a);
-            a = fmaf(xv[t][4], w1.x, a); a = fmaf(xv[t][5], w1.y, a);
-            a = fmaf(xv[t][6], w1.z, a); a = fmaf(xv[t][7], w1.w, a);
-            acc[t][e] = a;
+            const uint32_t u = kp == 0 ? xv[t].x : kp == 1 ? xv[t].y : kp == 2 ? xv[t].z : xv[t].w;
+            const float2 f = unpack_bf16x2(u);
+            xd0[t] = make_float2(f.x, f.x);
+            xd1[t] = make_float2(f.y, f.y);
+          }
+#pragma unroll
+          for (int ep = 0; ep < EP; ++ep) {
+            const float4 w = *reinterpret_cast<const float4*>(wrow + ep * 2 * hch + kp * 128);
+            const float2 w0 = make_float2(w.x, w.y), w1 = make_float2(w.z, w.w);
+#pragma unroll
+            for (int t = 0; t < TPW; ++t) {
+              ffma2(acc[t][ep], xd0[t], w0);
+              ffma2(acc[t][ep], xd1[t], w1);
+            }
           }
         }
       }
+      cp_async_wait_0();
     }
     // fixed butterfly over the 32 lanes (every lane ends with every sum)
 #pragma unroll
     for (int t = 0; t < TPW; ++t)
 #pragma unroll
-      for (int e = 0; e < EMAX; ++e) acc[t][e] = warp_sum(acc[t][e]);
+      for (int ep = 0; ep < EP; ++ep) {
+        acc[t][ep].x = warp_sum(acc[t][ep].x);
+        acc[t][ep].y = warp_sum(acc[t][ep].y);
+      }
     // lane t finalises token tok0 + t
 #pragma unroll
     for (int t = 0; t < TPW; ++t) {
       const int64_t tok = tok0 + t;
       if (lane != t || tok >= T) continue;
+      float lv[EMAX];
+#pragma unroll
+      for (int ep = 0; ep < EP; ++ep) {
+        lv[2 * ep] = acc[t][ep].x;
+        lv[2 * ep + 1] = acc[t][ep].y;
+      }
       float m = -FLT_MAX, m2 = -FLT_MAX;
       int best = 0;
 #pragma unroll
       for (int e = 0; e < EMAX; ++e) {
         if (e >= E) break;
-        const float v = acc[t][e];
+        const float v = lv[e];
         logits[(size_t)tok * E + e] = v;
         if (v > m) { m2 = m; m = v; best = e; }
         else if (v > m2) { m2 = v; }
@@ -121,13 +175,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
       for (int e = 0; e < EMAX; ++e) {
         if (e >= E) break;
-        den += expf(acc[t][e] - m);
+        den += expf(lv[e] - m);
       }
       const int chosen = forced ? forced[tok] : best;
       float lc = m;
 #pragma unroll
       for (int e = 0; e < EMAX; ++e)
-        if (e == chosen) lc = acc[t][e];
+        if (e == chosen) lc = lv[e];
       const float g = (E > 1) ? (m - m2) : FLT_MAX;
       expert[tok] = chosen;
       prob[tok] = expf(lc - m) / den;
@@ -207,11 +261,12 @@ cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
   constexpr int hmax = wg_chunk(EMAX);
   const int hpad = (a.H + 255) & ~255;
   const int hch = hpad < hmax ? hpad : hmax;
-  const int smem = EMAX * hch * 4;
+  const int smem = EMAX * hch * 4 + WARPS * 2 * TPW * 256 * 2;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gate_kernel<EMAX, TPW, WARPS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         128 * 1024 + WARPS * 2 * TPW * 256 * 2);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -239,11 +294,11 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s) {
     if (e == cudaSuccess) e = cudaMemsetAsync(a.load, 0, sizeof(int32_t) * a.E, s);
     return e;
   }
-  if (a.E <= 4) e = launch_gate<4, 8, 8>(a, s);
-  else if (a.E <= 8) e = launch_gate<8, 8, 8>(a, s);
-  else if (a.E <= 16) e = launch_gate<16, 4, 8>(a, s);
-  else if (a.E <= 32) e = launch_gate<32, 2, 8>(a, s);
-  else e = launch_gate<64, 1, 8>(a, s);
+  if (a.E <= 4) e = launch_gate<4, 4, 16>(a, s);
+  else if (a.E <= 8) e = launch_gate<8, 4, 16>(a, s);
+  else if (a.E <= 16) e = launch_gate<16, 4, 16>(a, s);
+  else if (a.E <= 32) e = launch_gate<32, 2, 16>(a, s);
+  else e = launch_gate<64, 1, 16>(a, s);
   if (e != cudaSuccess) return e;
   const int nblocks = (int)((a.T + SCAN_BLOCK - 1) / SCAN_BLOCK);
   slot_local_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.T, a.E, a.local_rank, a.block_hist);
