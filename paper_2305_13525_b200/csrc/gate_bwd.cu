@@ -67,7 +67,6 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int E = ss.E, H = ss.H;
-  const int64_t t0 = ((int64_t)blockIdx.x * DX_WARPS + warp) * 16;
   // H is split over gridDim.y CTAs (more warps in flight for this HBM-bound pass)
   const int ntiles_all = H / 8;
   const int per = ((ntiles_all + gridDim.y - 1) / gridDim.y + 7) & ~7;
@@ -81,6 +80,9 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
   }
   __syncthreads();
 
+  const int64_t nblocks = (T + 16 * DX_WARPS - 1) / (16 * DX_WARPS);
+  for (int64_t blkid = blockIdx.x; blkid < nblocks; blkid += gridDim.x) {
+  const int64_t t0 = (blkid * DX_WARPS + warp) * 16;
   uint32_t afr[KS][4];
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
       st_v4(dx + (size_t)(t0 + r) * H + h, o);
     }
     __syncwarp();
+  }
   }
 }
 
@@ -358,7 +361,13 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gate_bwd_dx_mma_kernel<EPK><<<dim3((unsigned)((T + tb - 1) / tb), hsplit), DX_WARPS * 32, smem, s>>>(
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t gx = (T + tb - 1) / tb;
+  const int64_t cap = (3 * (int64_t)sms + hsplit - 1) / hsplit;  // ~3 CTAs per SM, persistent
+  if (gx > cap) gx = cap;
+  gate_bwd_dx_mma_kernel<EPK><<<dim3((unsigned)gx, hsplit), DX_WARPS * 32, smem, s>>>(
       static_cast<const bf16*>(dS), wpk, logits, expert, slot, prob, dp, ss, T,
       static_cast<bf16*>(dx), dl);
   constexpr int NT = EP <= 32 ? 4 : 2;
