@@ -17,6 +17,12 @@
  * for each the F-slice [t*F/G_t, (t+1)*F/G_t): rows of W1 [F,H], columns of
  * W2 [H,F] (Megatron column/row split).
  *
+ * World > 1 (default exchange): the library owns peer-visible windows (cudaMalloc,
+ * CUDA-IPC mapped on every rank of the box): a ring of MOE_RING = 2 forward windows
+ * (expert inputs X and combine sources O) plus one backward pair. A saved blob is
+ * valid for backward while at most MOE_RING - 1 newer forwards ran on the ctx
+ * (else MOE_ERR_STATE).
+ *
  * Conventions for every call:
  *  - Tensor pointers are caller-owned CUDA device pointers unless stated;
  *    the library never allocates, frees or retains them past the call.
@@ -54,6 +60,8 @@ typedef enum {
 #define MOE_F_STATS 1u            /* keep the per-collective byte ledger (moe_stats)        */
 #define MOE_F_FORCED_ROUTING 2u   /* moe_forward takes forced_expert[T] instead of argmax   */
 #define MOE_F_TIMING 4u           /* record CUDA events around every kernel class (moe_stats) */
+#define MOE_F_NCCL_EXCHANGE 8u    /* EP exchange via NCCL send/recv + all-gather (baseline)
+                                     instead of the peer-memory copy kernel (default)       */
 
 /* Layer configuration. Identical on every rank of the job.
  * Constraints (checked, MOE_ERR_SHAPE otherwise):

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libmoe.so")
 MOE_F_STATS = 1
 MOE_F_FORCED_ROUTING = 2
 MOE_F_TIMING = 4
+MOE_F_NCCL_EXCHANGE = 8
 KERNEL_CLASSES = ("route", "dispatch", "gemm", "combine", "combine_bwd", "gate_bwd", "comm")
 COLL_NAMES = ("a2a", "allgather", "reducescatter", "allreduce")
 

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
@@ -35,6 +36,19 @@ struct moe_ctx {
   bool poisoned = false;
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
+  // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
+  enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, NWIN = 6 };
+  void* win[NWIN] = {};
+  std::vector<void*> opened;
+  void** d_table = nullptr;  // device [world][NWIN]
+  Piece* d_disp = nullptr;
+  Piece* d_ret = nullptr;
+  int n_disp = 0, n_ret = 0;
+  int64_t disp_bytes[3] = {0, 0, 0}, ret_bytes[3] = {0, 0, 0};  // by Piece::kind
+  float* d_barrier = nullptr;
+  uint64_t gen = 0;
+  uint64_t ring_gen[2] = {0, 0};
+  std::unordered_map<const void*, std::pair<int, uint64_t>> saved_slot;  // saved -> (ring slot, gen)
   const void* last_saved = nullptr;
   cudaStream_t last_stream = nullptr;
   // MOE_F_TIMING: event pairs per kernel class, resolved in moe_stats_get
@@ -236,6 +250,134 @@ moe_status gemm(moe_ctx* c, const GemmArgs& g, cudaStream_t st) {
   return MOE_OK;
 }
 
+
+// ---- peer-memory exchange (default for world > 1) ----
+// Piece lists (static per config): "dispatch" moves slot-space pieces (D, dO) into
+// expert-space windows (WX, WdY); "return" moves expert-space pieces (Ypart, dXp,
+// after the TP reduction) into slot-space windows (WO, WdS). Under DTD a rank
+// sends only its slot slice t, to every TP rank of the destination (the folded
+// all-gather); vanilla sends all slices to the same-t rank only.
+void build_pieces(const Dims& d, bool dispatch, std::vector<Piece>& v, int64_t bytes[3]) {
+  const uint64_t pb = (uint64_t)d.Cs * d.H * 2;
+  const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
+  auto rank_of = [&](int ep, int t) { return (d.d * d.Gep + ep) * d.Gt + t; };
+  auto push = [&](uint64_t so, uint64_t dof, int ep2, int t2) {
+    Piece p;
+    p.src_off = so;
+    p.dst_off = dof;
+    p.dst_rank = rank_of(ep2, t2);
+    p.kind = (p.dst_rank == d.rank) ? 0 : (t2 == d.t ? 1 : 2);
+    bytes[p.kind] += (int64_t)pb;
+    v.push_back(p);
+  };
+  for (int i = 0; i < 3; ++i) bytes[i] = 0;
+  if (dispatch) {
+    for (int e = 0; e < d.E; ++e) {
+      const int ep2 = e / d.El, el = e % d.El;
+      for (int tt = lo; tt < hi; ++tt) {
+        const uint64_t so = ((uint64_t)tt * d.E + e) * pb;
+        const uint64_t dof = (((uint64_t)el * d.Gt + tt) * d.Gep + d.ep) * pb;
+        if (d.dtd)
+          for (int t2 = 0; t2 < d.Gt; ++t2) push(so, dof, ep2, t2);
+        else
+          push(so, dof, ep2, d.t);
+      }
+    }
+  } else {
+    for (int el = 0; el < d.El; ++el) {
+      const int e = d.ep * d.El + el;
+      for (int src = 0; src < d.Gep; ++src)
+        for (int tt = lo; tt < hi; ++tt) {
+          const uint64_t so = (((uint64_t)el * d.Gt + tt) * d.Gep + src) * pb;
+          const uint64_t dof = ((uint64_t)tt * d.E + e) * pb;
+          if (d.dtd)
+            for (int t2 = 0; t2 < d.Gt; ++t2) push(so, dof, src, t2);
+          else
+            push(so, dof, src, d.t);
+        }
+    }
+  }
+}
+
+moe_status setup_peer(moe_ctx* c) {
+  const Dims& d = c->d;
+  const size_t expert_space = (size_t)d.El * d.R * d.H * 2;
+  const size_t slot_space = (size_t)d.E * d.C * d.H * 2;
+  const size_t sizes[moe_ctx::NWIN] = {expert_space, expert_space, slot_space, slot_space,
+                                       expert_space, slot_space};
+  std::vector<cudaIpcMemHandle_t> mine(moe_ctx::NWIN);
+  for (int w = 0; w < moe_ctx::NWIN; ++w) {
+    CUDA_TRY(c, cudaMalloc(&c->win[w], sizes[w]));
+    CUDA_TRY(c, cudaMemset(c->win[w], 0, sizes[w]));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&mine[w], c->win[w]));
+  }
+  const size_t hb = sizeof(cudaIpcMemHandle_t) * moe_ctx::NWIN;
+  uint8_t* dbuf = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dbuf, hb * d.world));
+  CUDA_TRY(c, cudaMemcpy(dbuf + hb * d.rank, mine.data(), hb, cudaMemcpyHostToDevice));
+  cudaStream_t st;
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  NCCL_TRY(c, ncclAllGather(dbuf + hb * d.rank, dbuf, hb, ncclUint8, c->world_comm, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  std::vector<cudaIpcMemHandle_t> all(moe_ctx::NWIN * d.world);
+  CUDA_TRY(c, cudaMemcpy(all.data(), dbuf, hb * d.world, cudaMemcpyDeviceToHost));
+  cudaFree(dbuf);
+  std::vector<void*> table((size_t)d.world * moe_ctx::NWIN, nullptr);
+  for (int r = 0; r < d.world; ++r)
+    for (int w = 0; w < moe_ctx::NWIN; ++w) {
+      if (r == d.rank) {
+        table[(size_t)r * moe_ctx::NWIN + w] = c->win[w];
+        continue;
+      }
+      void* p = nullptr;
+      CUDA_TRY(c, cudaIpcOpenMemHandle(&p, all[(size_t)r * moe_ctx::NWIN + w],
+                                       cudaIpcMemLazyEnablePeerAccess));
+      c->opened.push_back(p);
+      table[(size_t)r * moe_ctx::NWIN + w] = p;
+    }
+  CUDA_TRY(c, cudaMalloc(&c->d_table, sizeof(void*) * table.size()));
+  CUDA_TRY(c, cudaMemcpy(c->d_table, table.data(), sizeof(void*) * table.size(), cudaMemcpyHostToDevice));
+  std::vector<Piece> disp, ret;
+  build_pieces(d, true, disp, c->disp_bytes);
+  build_pieces(d, false, ret, c->ret_bytes);
+  c->n_disp = (int)disp.size();
+  c->n_ret = (int)ret.size();
+  CUDA_TRY(c, cudaMalloc(&c->d_disp, sizeof(Piece) * (disp.size() + 1)));
+  CUDA_TRY(c, cudaMalloc(&c->d_ret, sizeof(Piece) * (ret.size() + 1)));
+  CUDA_TRY(c, cudaMemcpy(c->d_disp, disp.data(), sizeof(Piece) * disp.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy(c->d_ret, ret.data(), sizeof(Piece) * ret.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMalloc(&c->d_barrier, sizeof(float)));
+  CUDA_TRY(c, cudaMemset(c->d_barrier, 0, sizeof(float)));
+  CUDA_TRY(c, cudaStreamDestroy(st));
+  return MOE_OK;
+}
+
+void teardown_peer(moe_ctx* c) {
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  c->opened.clear();
+  for (int w = 0; w < moe_ctx::NWIN; ++w)
+    if (c->win[w]) cudaFree(c->win[w]);
+  if (c->d_table) cudaFree(c->d_table);
+  if (c->d_disp) cudaFree(c->d_disp);
+  if (c->d_ret) cudaFree(c->d_ret);
+  if (c->d_barrier) cudaFree(c->d_barrier);
+}
+
+// One exchange + the cross-rank barrier that publishes it (every writer's copy
+// kernel precedes its barrier contribution in stream order).
+moe_status exchange(moe_ctx* c, bool dispatch, int pass, const void* src, int win, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t pb = (size_t)d.Cs * d.H * 2;
+  CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, dispatch ? c->d_disp : c->d_ret,
+                            dispatch ? c->n_disp : c->n_ret, pb, st));
+  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  NCCL_TRY(c, ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclFloat32, ncclSum, c->world_comm, st));
+  const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
+  if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
+  if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);
+  return MOE_OK;
+}
+
 #define TRY(expr)                         \
   do {                                    \
     moe_status _s = (expr);               \
@@ -349,6 +491,18 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
       delete c;
       return fail(MOE_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
     }
+    if (d.peer) {
+      moe_status ps = setup_peer(c);
+      if (ps != MOE_OK) {
+        const std::string why2 = g_detail;
+        teardown_peer(c);
+        if (c->tp_comm) ncclCommDestroy(c->tp_comm);
+        if (c->ep_comm) ncclCommDestroy(c->ep_comm);
+        ncclCommDestroy(c->world_comm);
+        delete c;
+        return fail(ps, "peer-memory exchange setup: " + why2);
+      }
+    }
   }
   *out = c;
   return MOE_OK;
@@ -356,6 +510,10 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
 
 moe_status moe_destroy(moe_ctx* c) {
   if (!c) return MOE_OK;
+  if (c->d.peer) {
+    cudaDeviceSynchronize();
+    teardown_peer(c);
+  }
   if (c->tp_comm) ncclCommDestroy(c->tp_comm);
   if (c->ep_comm) ncclCommDestroy(c->ep_comm);
   if (c->world_comm) ncclCommDestroy(c->world_comm);
@@ -400,8 +558,12 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
     CUDA_TRY(c, route(ra, st));
   }
 
+  // ring slot of the peer windows used by this forward
+  const int rslot = (int)(c->gen & 1);
+  const uint64_t mygen = ++c->gen;
+
   // F3 dispatch (DTD: only this rank's slot slice), F4 a2a, F5 all-gather
-  void* X = at<uint8_t>(saved, sv.X);
+  void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
   void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
   {
     Scope sc_(c, MOE_K_DISPATCH, st, 1);
@@ -409,14 +571,18 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   }
   if (!solo) {
     Scope sc_(c, MOE_K_COMM, st, 0);
-    TRY(ep_exchange(c, 0, 0, D, X, lo, hi, st));
-    if (d.dtd) TRY(ag_expert(c, 0, X, st));
+    if (d.peer) {
+      TRY(exchange(c, true, 0, D, moe_ctx::W_X0 + rslot, st));
+    } else {
+      TRY(ep_exchange(c, 0, 0, D, X, lo, hi, st));
+      if (d.dtd) TRY(ag_expert(c, 0, X, st));
+    }
   }
 
   // F6 GEMM1 + GeLU, F7 GEMM2
   void* Hpre = at<uint8_t>(saved, sv.Hpre);
   void* A = at<uint8_t>(saved, sv.A);
-  void* O = at<uint8_t>(saved, sv.O);
+  void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
   void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
   GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, Hpre, EPI_GELU, A};
   TRY(gemm(c, g1, st));
@@ -430,8 +596,12 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
       if (d.dtd) TRY(rs_expert(c, 0, Y, st));
       else TRY(ar_expert(c, 0, Y, st));
     }
-    TRY(ep_exchange(c, 1, 0, O, Y, lo, hi, st));
-    if (d.dtd) TRY(ag_slot(c, 0, O, st));
+    if (d.peer) {
+      TRY(exchange(c, false, 0, Y, moe_ctx::W_O0 + rslot, st));
+    } else {
+      TRY(ep_exchange(c, 1, 0, O, Y, lo, hi, st));
+      if (d.dtd) TRY(ag_slot(c, 0, O, st));
+    }
   }
 
   // F11 combine
@@ -440,6 +610,8 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
     CUDA_TRY(c, combine(O, ra.expert, ra.slot, ra.prob, ss, d.T, y, st));
   }
   c->saved_written.insert(saved);
+  c->saved_slot[saved] = {rslot, mygen};
+  c->ring_gen[rslot] = mygen;
   c->last_saved = saved;
   c->last_stream = st;
   return MOE_OK;
@@ -454,6 +626,14 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     return fail(MOE_ERR_ARG, "null tensor pointer");
   if (!c->saved_written.count(saved))
     return fail(MOE_ERR_STATE, "saved blob was not written by moe_forward on this ctx");
+  int rslot = 0;
+  if (c->d.peer) {
+    const auto it = c->saved_slot.find(saved);
+    if (it == c->saved_slot.end() || c->ring_gen[it->second.first] != it->second.second)
+      return fail(MOE_ERR_STATE, "saved blob's peer window was reused: more than 1 newer forward ran "
+                                 "before this backward (ring of 2)");
+    rslot = it->second.first;
+  }
   if (!aligned16(dy) || !aligned16(x) || !aligned16(wg) || !aligned16(w1) || !aligned16(w2) ||
       !aligned16(dx) || !aligned16(dwg) || !aligned16(dw1) || !aligned16(dw2))
     return fail(MOE_ERR_ALIGN, "tensor pointers must be 16-byte aligned");
@@ -469,16 +649,16 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   const float* prob = at<float>(saved, sv.prob);
   const float* logits = at<float>(saved, sv.logits);
   const int32_t* count = at<int32_t>(saved, sv.count);
-  const void* X = at<uint8_t>(saved, sv.X);
+  const void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
   const void* Hpre = at<uint8_t>(saved, sv.Hpre);
   const void* A = at<uint8_t>(saved, sv.A);
-  const void* O = at<uint8_t>(saved, sv.O);
+  const void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
   float* dp = at<float>(c->scratch, sc.dp);
-  void* dY = at<uint8_t>(c->scratch, sc.dY);
+  void* dY = d.peer ? c->win[moe_ctx::W_DY] : at<uint8_t>(c->scratch, sc.dY);
   void* dO = at<uint8_t>(c->scratch, sc.dO);
   void* dH = at<uint8_t>(c->scratch, sc.dH);
   void* dXp = at<uint8_t>(c->scratch, sc.dXp);
-  void* dS = at<uint8_t>(c->scratch, sc.dS);
+  void* dS = d.peer ? c->win[moe_ctx::W_DS] : at<uint8_t>(c->scratch, sc.dS);
 
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
   {
@@ -487,8 +667,12 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   }
   if (!solo) {
     Scope sc_(c, MOE_K_COMM, st, 0);
-    TRY(ep_exchange(c, 0, 1, dO, dY, lo, hi, st));
-    if (d.dtd) TRY(ag_expert(c, 1, dY, st));
+    if (d.peer) {
+      TRY(exchange(c, true, 1, dO, moe_ctx::W_DY, st));
+    } else {
+      TRY(ep_exchange(c, 0, 1, dO, dY, lo, hi, st));
+      if (d.dtd) TRY(ag_expert(c, 1, dY, st));
+    }
   }
   // B4 dHpre = (dY W2) * gelu'(Hpre); B5 dXpart = dHpre W1; B6 dW2 = dY^T A, dW1 = dHpre^T X
   GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(Hpre)};
@@ -506,8 +690,12 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       if (d.dtd) TRY(rs_expert(c, 1, dXp, st));
       else TRY(ar_expert(c, 1, dXp, st));
     }
-    TRY(ep_exchange(c, 1, 1, dS, dXp, lo, hi, st));
-    if (d.dtd) TRY(ag_slot(c, 1, dS, st));
+    if (d.peer) {
+      TRY(exchange(c, false, 1, dXp, moe_ctx::W_DS, st));
+    } else {
+      TRY(ep_exchange(c, 1, 1, dS, dXp, lo, hi, st));
+      if (d.dtd) TRY(ag_slot(c, 1, dS, st));
+    }
   }
   // B10 dispatch-bwd + gate-bwd
   {

@@ -81,4 +81,14 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
 int gate_bwd_splits(int64_t T);
 size_t gate_bwd_pack_bytes(int H, int E);
 
+// (peer.cu) one piece of a peer-memory exchange: C_s x H bytes from src + src_off to
+// window `win` of rank dst_rank at dst_off. kind: 0 local, 1 a2a (EP peer), 2 folded
+// all-gather (TP peer) — used only by the byte ledger.
+struct Piece {
+  uint64_t src_off, dst_off;
+  int32_t dst_rank, kind;
+};
+cudaError_t peer_exchange(const void* src, void* const* d_table, int nwin, int win,
+                          const Piece* d_pieces, int npieces, size_t piece_bytes, cudaStream_t s);
+
 }  // namespace moe

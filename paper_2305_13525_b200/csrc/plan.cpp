@@ -26,7 +26,7 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   const int tp_ep = c->g_tensor * c->g_expert;
   if (world % tp_ep) { *why = "world % (g_tensor * g_expert) != 0"; return MOE_ERR_SHAPE; }
   if (c->tokens > (int64_t)1 << 30) { *why = "tokens must be < 2^30"; return MOE_ERR_SHAPE; }
-  if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING)) { *why = "unknown flag bits"; return MOE_ERR_ARG; }
+  if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING | MOE_F_NCCL_EXCHANGE)) { *why = "unknown flag bits"; return MOE_ERR_ARG; }
   d->T = c->tokens;
   d->H = c->hidden;
   d->F = c->ffn;
@@ -51,6 +51,7 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->S = world / d->Gt;
   d->dtd = c->dtd != 0 && d->Gt > 1;
   d->forced = (c->flags & MOE_F_FORCED_ROUTING) != 0;
+  d->peer = world > 1 && (c->flags & MOE_F_NCCL_EXCHANGE) == 0;
   if (d->R > (int64_t)1 << 30) { *why = "rows per expert too large"; return MOE_ERR_SHAPE; }
   return MOE_OK;
 }
@@ -80,10 +81,11 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sv->load = s.take((size_t)d.E * 4);
   sv->ties = s.take(4);
   sv->tok_of = s.take((size_t)d.E * d.C * 4);
-  sv->X = s.take(expert_space);
+  // peer mode keeps X and O in the library's ring windows instead of the saved blob
+  sv->X = d.peer ? 0 : s.take(expert_space);
   sv->Hpre = s.take(ffn_space);
   sv->A = s.take(ffn_space);
-  sv->O = s.take(slot_space);
+  sv->O = d.peer ? 0 : s.take(slot_space);
   sv->total = s.off;
 
   const bool solo = d.world == 1;  // slot space == expert space, no communication
@@ -102,11 +104,11 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dl = b.take((size_t)d.T * d.E * 4);
   sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));
-  sc->dY = b.take(expert_space);
+  sc->dY = d.peer ? 0 : b.take(expert_space);   // peer mode: window WdY
   sc->dO = solo ? sc->dY : b.take(slot_space);
   sc->dH = b.take(ffn_space);
   sc->dXp = b.take(expert_space);
-  sc->dS = solo ? sc->dXp : b.take(slot_space);
+  sc->dS = solo ? sc->dXp : (d.peer ? 0 : b.take(slot_space));  // peer mode: window WdS
   sc->total = f.off > b.off ? f.off : b.off;
 }
 

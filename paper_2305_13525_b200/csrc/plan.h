@@ -22,6 +22,7 @@ struct Dims {
   int S;             // token groups
   bool dtd;          // DTD in effect (requested and G_t > 1)
   bool forced;
+  bool peer;         // world > 1 and the peer-memory exchange (not MOE_F_NCCL_EXCHANGE)
 };
 
 // Validates and derives; returns MOE_OK or an error with *why set.

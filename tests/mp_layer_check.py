@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import moe_oracle as O  # noqa: E402
-from paper_2305_13525_b200 import MoEConfig, MoELayer, synth  # noqa: E402
+from paper_2305_13525_b200 import MOE_F_NCCL_EXCHANGE, MoEConfig, MoELayer, synth  # noqa: E402
 from tests.helpers import REL_L2_BAR, bf16_tensor, rel_l2, tensor_f64  # noqa: E402
 
 
@@ -58,8 +58,12 @@ def main():
     w1_b, w2_b = synth.make_experts(shape)
 
     results = {}
-    for dtd in (True, False):
+    for mode in ((True, False), (False, False), (True, True)):  # (dtd, nccl exchange)
+        dtd, nccl = mode
         cfg = MoEConfig.from_shape(shape, dtd=dtd)
+        if nccl:
+            cfg = MoEConfig(cfg.tokens, cfg.hidden, cfg.ffn, cfg.experts, cfg.capacity_factor,
+                            cfg.g_tensor, cfg.g_expert, cfg.dtd, cfg.flags | MOE_F_NCCL_EXCHANGE)
         layer = MoELayer(cfg, world, rank, dev)
         L = layer.layout
         s = L["d"] * a.gep + L["ep"]
@@ -74,7 +78,8 @@ def main():
         rt = layer.moe_routing(saved)
         torch.cuda.synchronize()
         st = layer.moe_stats()
-        results[dtd] = {"y": y.clone(), "dx": dx.clone(), "dwg": dwg.clone(), "dw1": dw1.clone(),
+        key = "nccl" if nccl else dtd
+        results[key] = {"y": y.clone(), "dx": dx.clone(), "dwg": dwg.clone(), "dw1": dw1.clone(),
                         "dw2": dw2.clone(), "rt": {k: v.cpu().numpy() for k, v in rt.items()},
                         "stats": st, "layout": L, "group": s}
         layer.close()
@@ -134,6 +139,13 @@ def main():
             failures.append(f"DTD != vanilla (bitwise) for {k}")
         if not same and rel_l2(tensor_f64(v[k]), tensor_f64(t_[k])) > 1e-2:
             failures.append(f"DTD vs vanilla differ for {k}")
+    # ---- peer-memory exchange vs NCCL exchange (same arithmetic, same positions)
+    nc = results["nccl"]
+    for k in ("y", "dx", "dwg", "dw1", "dw2"):
+        if not torch.equal(nc[k], t_[k]):
+            failures.append(f"peer exchange != NCCL exchange (bitwise) for {k}")
+    if nc["stats"]["wire_bytes"] != t_["stats"]["wire_bytes"]:
+        failures.append(f"ledger differs: peer {t_['stats']['wire_bytes']} nccl {nc['stats']['wire_bytes']}")
     a2a_dtd = t_["stats"]["wire_bytes"]["a2a"]
     a2a_van = v["stats"]["wire_bytes"]["a2a"]
     if a2a_dtd * a.gt != a2a_van:
