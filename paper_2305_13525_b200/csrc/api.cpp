@@ -363,6 +363,27 @@ void teardown_peer(moe_ctx* c) {
   if (c->d_barrier) cudaFree(c->d_barrier);
 }
 
+PeerDst peer_dst(const moe_ctx* c, int win) {
+  const Dims& d = c->d;
+  PeerDst pd;
+  pd.table = c->d_table;
+  pd.nwin = moe_ctx::NWIN;
+  pd.win = win;
+  pd.d = d.d; pd.ep = d.ep; pd.t = d.t; pd.Gt = d.Gt; pd.Gep = d.Gep; pd.El = d.El;
+  pd.dtd = d.dtd ? 1 : 0;
+  return pd;
+}
+
+// Barrier publishing a fused peer write (dispatch / combine-backward) + ledger.
+moe_status publish(moe_ctx* c, bool dispatch, int pass, cudaStream_t st) {
+  const Dims& d = c->d;
+  NCCL_TRY(c, ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclFloat32, ncclSum, c->world_comm, st));
+  const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
+  if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
+  if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);
+  return MOE_OK;
+}
+
 // One exchange + the cross-rank barrier that publishes it (every writer's copy
 // kernel precedes its barrier contribution in stream order).
 moe_status exchange(moe_ctx* c, bool dispatch, int pass, const void* src, int win, cudaStream_t st) {
@@ -565,15 +586,21 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   // F3 dispatch (DTD: only this rank's slot slice), F4 a2a, F5 all-gather
   void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
   void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
-  {
+  if (d.peer) {
+    // fused: rows go straight from x into the peers' expert-space windows
+    {
+      Scope sc_(c, MOE_K_DISPATCH, st, 1);
+      CUDA_TRY(c, dispatch_peer(x, ra.tok_of, ra.count, ss, lo, hi, peer_dst(c, moe_ctx::W_X0 + rslot), st));
+    }
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(publish(c, true, 0, st));
+  } else {
     Scope sc_(c, MOE_K_DISPATCH, st, 1);
     CUDA_TRY(c, dispatch(x, ra.tok_of, ra.count, ss, lo, hi, D, st));
   }
-  if (!solo) {
+  if (!solo && !d.peer) {
     Scope sc_(c, MOE_K_COMM, st, 0);
-    if (d.peer) {
-      TRY(exchange(c, true, 0, D, moe_ctx::W_X0 + rslot, st));
-    } else {
+    {
       TRY(ep_exchange(c, 0, 0, D, X, lo, hi, st));
       if (d.dtd) TRY(ag_expert(c, 0, X, st));
     }
@@ -661,15 +688,21 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   void* dS = d.peer ? c->win[moe_ctx::W_DS] : at<uint8_t>(c->scratch, sc.dS);
 
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
-  {
+  if (d.peer) {
+    {
+      Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
+      CUDA_TRY(c, combine_bwd_peer(dy, O, expert, slot, prob, count, nullptr, ss, d.T, lo, hi, dp,
+                                   peer_dst(c, moe_ctx::W_DY), st));
+    }
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(publish(c, true, 1, st));
+  } else {
     Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
     CUDA_TRY(c, combine_bwd(dy, O, expert, slot, prob, count, ss, d.T, lo, hi, dp, dO, st));
   }
-  if (!solo) {
+  if (!solo && !d.peer) {
     Scope sc_(c, MOE_K_COMM, st, 0);
-    if (d.peer) {
-      TRY(exchange(c, true, 1, dO, moe_ctx::W_DY, st));
-    } else {
+    {
       TRY(ep_exchange(c, 0, 1, dO, dY, lo, hi, st));
       if (d.dtd) TRY(ag_expert(c, 1, dY, st));
     }

@@ -91,4 +91,23 @@ struct Piece {
 cudaError_t peer_exchange(const void* src, void* const* d_table, int nwin, int win,
                           const Piece* d_pieces, int npieces, size_t piece_bytes, cudaStream_t s);
 
+// Destination of slot-space rows in the expert-space windows of the EP/TP peers
+// (fused dispatch / combine-backward): slot (tt, e, cs) of this rank lands at
+// [el][tt][ep][cs] of rank (d, e / E_l, t') for t' in {t} (vanilla) or all t' (DTD).
+struct PeerDst {
+  void* const* table;  // device [world][nwin]
+  int nwin, win;
+  int d, ep, t, Gt, Gep, El;
+  int dtd;
+};
+// F3 + F4 (+F5): gather x rows of slices [t_lo, t_hi) straight into the peers' windows.
+cudaError_t dispatch_peer(const void* x, const int32_t* tok_of, const int32_t* count,
+                          const SlotSpace& ss, int t_lo, int t_hi, const PeerDst& pd,
+                          cudaStream_t s);
+// B1 + B2 (+B3): dp_t and dO rows (p_t dy_t, zeros for empty slots) straight into the peers' windows.
+cudaError_t combine_bwd_peer(const void* dy, const void* O, const int32_t* expert,
+                             const int32_t* slot, const float* prob, const int32_t* count,
+                             const int32_t* tok_of, const SlotSpace& ss, int64_t T, int t_lo,
+                             int t_hi, float* dp, const PeerDst& pd, cudaStream_t s);
+
 }  // namespace moe

@@ -169,6 +169,139 @@ __global__ void __launch_bounds__(WARPS * 32)
   copy_row<true>(nullptr, D + ((size_t)(tt * ss.E + e) * ss.Cs + cs) * ss.H, ss.H / 8, lane);
 }
 
+
+// ---------------------------------------------------------------- fused peer variants
+__device__ __forceinline__ uint8_t* peer_row(const PeerDst& pd, int tt, int e, int64_t cs,
+                                             const SlotSpace& ss, int t2) {
+  const int ep2 = e / pd.El, el = e % pd.El;
+  const int r = (pd.d * pd.Gep + ep2) * pd.Gt + t2;
+  uint8_t* base = static_cast<uint8_t*>(pd.table[(size_t)r * pd.nwin + pd.win]);
+  return base + ((((size_t)el * pd.Gt + tt) * pd.Gep + pd.ep) * ss.Cs + cs) * ss.H * 2;
+}
+
+// One warp per slot row: the x row (or zeros) is read once and stored to every
+// destination rank (1 for vanilla, G_t for DTD) with 16-byte stores over NVLink.
+__global__ void __launch_bounds__(WARPS * 32)
+    dispatch_peer_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ tok_of,
+                         const int32_t* __restrict__ count, SlotSpace ss, int t_lo, int64_t rows,
+                         PeerDst pd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t per_slice = (int64_t)ss.E * ss.Cs;
+  const int tt = t_lo + (int)(r / per_slice);
+  const int64_t rem = r % per_slice;
+  const int e = (int)(rem / ss.Cs);
+  const int64_t cs = rem % ss.Cs;
+  const int64_t c = (int64_t)tt * ss.Cs + cs;
+  const int nv = ss.H / 8;
+  const bool full = c < count[e];
+  const bf16* src = full ? x + (size_t)tok_of[(size_t)e * ss.C + c] * ss.H : nullptr;
+  const int nd = pd.dtd ? pd.Gt : 1;
+  constexpr int U = 8;
+  for (int v0 = 0; v0 < nv; v0 += 32 * U) {
+    uint4 buf[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * 32 + lane;
+      buf[u] = (full && v < nv) ? ld_nc_v4(src + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+    }
+    for (int k = 0; k < nd; ++k) {
+      bf16* dst = reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nv) st_v4(dst + (size_t)v * 8, buf[u]);
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// Token-parallel: dp_t = <dy_t, O[row(t)]>; for kept tokens whose slot is in
+// slices [t_lo, t_hi), the row p_t dy_t is stored to every destination rank.
+__global__ void __launch_bounds__(WARPS * 32)
+    combine_bwd_peer_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ O,
+                            const int32_t* __restrict__ expert, const int32_t* __restrict__ slot,
+                            const float* __restrict__ prob, SlotSpace ss, int64_t T, int t_lo,
+                            int t_hi, float* __restrict__ dp, PeerDst pd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int s = slot[t];
+  if (s < 0) {
+    if (lane == 0) dp[t] = 0.f;
+    return;
+  }
+  const int e = expert[t];
+  const size_t row = slot_row(ss, e, s);
+  const int tt = (int)(s / ss.Cs);
+  const int64_t cs = s - (int64_t)tt * ss.Cs;
+  const bool mine = tt >= t_lo && tt < t_hi;
+  const float p = prob[t];
+  const bf16* dyr = dy + (size_t)t * ss.H;
+  const bf16* orow = O + row;
+  const int nv = ss.H / 8;
+  const int nd = mine ? (pd.dtd ? pd.Gt : 1) : 0;
+  float acc = 0.f;
+  constexpr int U = 4;
+  for (int v0 = 0; v0 < nv; v0 += 32 * U) {
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u * 32 + lane;
+      a[u] = v < nv ? ld_nc_v4(dyr + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+      b[u] = v < nv ? ld_nc_v4(orow + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+    }
+    uint4 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t wa[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+      uint32_t wb[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 fa = unpack_bf16x2(wa[k]), fb = unpack_bf16x2(wb[k]);
+        acc = fmaf(fa.x, fb.x, acc);
+        acc = fmaf(fa.y, fb.y, acc);
+        o[k] = pack_bf16x2(p * fa.x, p * fa.y);
+      }
+      w[u] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    for (int k = 0; k < nd; ++k) {
+      bf16* dst = reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nv) st_v4(dst + (size_t)v * 8, w[u]);
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) dp[t] = acc;
+  __threadfence_system();
+}
+
+// zero rows for the empty slots (c >= count[e]) of slices [t_lo, t_hi) in the peers' windows
+__global__ void __launch_bounds__(WARPS * 32)
+    zero_empty_peer_kernel(const int32_t* __restrict__ count, SlotSpace ss, int t_lo, int64_t rows,
+                           PeerDst pd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int64_t per_slice = (int64_t)ss.E * ss.Cs;
+  const int tt = t_lo + (int)(r / per_slice);
+  const int64_t rem = r % per_slice;
+  const int e = (int)(rem / ss.Cs);
+  const int64_t cs = rem % ss.Cs;
+  if ((int64_t)tt * ss.Cs + cs < count[e]) return;
+  const int nd = pd.dtd ? pd.Gt : 1;
+  for (int k = 0; k < nd; ++k)
+    copy_row<true>(nullptr, reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)),
+                   ss.H / 8, lane);
+  __threadfence_system();
+}
+
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + WARPS - 1) / WARPS); }
 
 }  // namespace
@@ -202,6 +335,32 @@ cudaError_t combine_bwd(const void* dy, const void* O, const int32_t* expert, co
   if (rows > 0)
     zero_empty_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(count, ss, t_lo, rows,
                                                                static_cast<bf16*>(dO));
+  return cudaGetLastError();
+}
+
+
+cudaError_t dispatch_peer(const void* x, const int32_t* tok_of, const int32_t* count,
+                          const SlotSpace& ss, int t_lo, int t_hi, const PeerDst& pd,
+                          cudaStream_t s) {
+  const int64_t rows = (int64_t)(t_hi - t_lo) * ss.E * ss.Cs;
+  if (rows <= 0) return cudaSuccess;
+  dispatch_peer_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(static_cast<const bf16*>(x), tok_of,
+                                                                count, ss, t_lo, rows, pd);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_bwd_peer(const void* dy, const void* O, const int32_t* expert,
+                             const int32_t* slot, const float* prob, const int32_t* count,
+                             const int32_t* tok_of, const SlotSpace& ss, int64_t T, int t_lo,
+                             int t_hi, float* dp, const PeerDst& pd, cudaStream_t s) {
+  (void)tok_of;
+  if (T > 0)
+    combine_bwd_peer_kernel<<<blocks_for(T), WARPS * 32, 0, s>>>(
+        static_cast<const bf16*>(dy), static_cast<const bf16*>(O), expert, slot, prob, ss, T, t_lo,
+        t_hi, dp, pd);
+  const int64_t rows = (int64_t)(t_hi - t_lo) * ss.E * ss.Cs;
+  if (rows > 0)
+    zero_empty_peer_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(count, ss, t_lo, rows, pd);
   return cudaGetLastError();
 }
 

@@ -97,7 +97,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   Bump f;
   sc->local_rank = f.take((size_t)d.T * 4);
   sc->block_hist = f.take((size_t)((d.T + 1023) / 1024) * d.E * 4);
-  sc->D = solo ? 0 : f.take(slot_space);
+  sc->D = (solo || d.peer) ? 0 : f.take(slot_space);  // peer mode dispatches straight into windows
   sc->Ypart = solo ? 0 : f.take(expert_space);
   Bump b;  // backward region reuses the forward region
   sc->dp = b.take((size_t)d.T * 4);
@@ -105,7 +105,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));
   sc->dY = d.peer ? 0 : b.take(expert_space);   // peer mode: window WdY
-  sc->dO = solo ? sc->dY : b.take(slot_space);
+  sc->dO = solo ? sc->dY : (d.peer ? 0 : b.take(slot_space));
   sc->dH = b.take(ffn_space);
   sc->dXp = b.take(expert_space);
   sc->dS = solo ? sc->dXp : (d.peer ? 0 : b.take(slot_space));  // peer mode: window WdS
