@@ -344,3 +344,51 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 }  // namespace moe
+
+namespace moe {
+
+// ---------------------------------------------------------------- packed fp32 epilogue math
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2f(unsigned long long u) { return *reinterpret_cast<float2*>(&u); }
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(d);
+}
+
+// gelu_tanh on a pair (same formula as gelu_f)
+__device__ __forceinline__ float2 gelu2(float2 h) {
+  const float k = 0.7978845608028654f, c = 0.044715f;
+  const float2 h2 = f2mul(h, h);
+  const float2 t = f2fma(h2, make_float2(c, c), make_float2(1.f, 1.f));  // 1 + c h^2
+  const float2 u = f2mul(f2mul(h, make_float2(k, k)), t);
+  const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 hh = f2mul(h, make_float2(0.5f, 0.5f));
+  return f2fma(hh, th, hh);  // 0.5 h (1 + tanh u)
+}
+
+// d gelu_tanh / dh on a pair (same formula as gelu_grad_f)
+__device__ __forceinline__ float2 gelu_grad2(float2 h) {
+  const float k = 0.7978845608028654f, c = 0.044715f;
+  const float2 h2 = f2mul(h, h);
+  const float2 t = f2fma(h2, make_float2(c, c), make_float2(1.f, 1.f));
+  const float2 kh = f2mul(h, make_float2(k, k));
+  const float2 u = f2mul(kh, t);
+  const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 a = f2fma(th, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));            // 0.5 (1 + th)
+  const float2 s = f2fma(f2mul(th, th), make_float2(-1.f, -1.f), make_float2(1.f, 1.f));   // 1 - th^2
+  const float2 b = f2fma(h2, make_float2(3.f * c, 3.f * c), make_float2(1.f, 1.f));         // 1 + 3 c h^2
+  return f2fma(f2mul(f2mul(kh, make_float2(0.5f, 0.5f)), s), b, a);
+}
+
+}  // namespace moe

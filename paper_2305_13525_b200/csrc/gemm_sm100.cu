@@ -270,13 +270,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // MMAs; both CTAs' TMA loads count on the leader's full barrier; commits are
 // multicast to both CTAs; each CTA's epilogue drains its own 128 TMEM lanes and
 // both arrive on the leader's tmem-empty barrier.
-constexpr int STAGES2 = 6;
 constexpr int A2_STAGE = 128 * BK * 2;  // 16 KiB
 constexpr int B2_STAGE = 128 * BK * 2;  // 16 KiB (this CTA's half of BN = 256)
+constexpr int EPI_WARPS = 8;            // 2 per TMEM lane quadrant, each half of the 256 columns
+constexpr int NUM_THREADS2 = (4 + EPI_WARPS) * 32;
 constexpr int EPI_BUF = 32 * 32 * 2;  // one warp's 32 x 32 bf16 chunk, 64B-swizzled
-// per epilogue warp: 2 buffers for D and 2 for the GeLU output
-constexpr int EPI_SMEM = 4 * 4 * EPI_BUF;  // 32 KiB
-constexpr int SMEM2_BYTES = STAGES2 * (A2_STAGE + B2_STAGE) + EPI_SMEM + 1024 + 256;
+// per epilogue warp: 2 staging buffers per output (D, and A = gelu for EPI_GELU);
+// the two-output GeLU variant gives up one pipeline stage to fit
+__host__ __device__ constexpr int epi_outs(int epi) { return epi == EPI_GELU ? 2 : 1; }
+__host__ __device__ constexpr int stages2(int epi) { return epi == EPI_GELU ? 5 : 6; }
+__host__ __device__ constexpr int epi_smem(int epi) { return EPI_WARPS * 2 * epi_outs(epi) * EPI_BUF; }
+__host__ __device__ constexpr int smem2_bytes(int epi) {
+  return stages2(epi) * (A2_STAGE + B2_STAGE) + epi_smem(epi) + 1024 + 256;
+}
 
 __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
@@ -284,10 +290,12 @@ __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
 }
 
 template <int A_MN, int B_MN, int EPI>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                  const Params p) {
+  constexpr int STAGES2 = stages2(EPI);
+  constexpr int EPI_SMEM = epi_smem(EPI);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -316,7 +324,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
-      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
     }
     fence_barrier_init();
   }
@@ -406,8 +414,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // 32 rows x 32 cols -> TMA bulk-tensor store (coalesced; rows >= M and
     // columns >= N are clipped by the tensor map). Two buffers per output per
     // warp; a buffer is rewritten only after its previous store has been read.
-    const int quad = warp & 3;
-    const uint32_t ebase = smem_u32(smE) + quad * 4 * EPI_BUF;
+    const int ew = warp - 4;
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
+    const int col0 = (ew >> 2) * (BN / 2);  // this warp's half of the columns
+    constexpr int NO = epi_outs(EPI);
+    const uint32_t ebase = smem_u32(smE) + ew * 2 * NO * EPI_BUF;
     const uint32_t swz = (uint32_t)((lane >> 1) & 3);
     int iter = 0, chunk_ctr = 0;
     for (int tile = cluster; tile < p.total_tiles; tile += nclusters, ++iter) {
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool row_ok = m < p.M;
       const size_t row_off = ((size_t)b * p.M + (row_ok ? m : 0)) * (size_t)p.N;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = col0; c < col0 + BN / 2; c += 32) {
         const int n = n0 + c;
         if (n >= p.N) break;  // uniform across the warp
         uint32_t v[32];
@@ -440,15 +451,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t o[16], g[16];
 #pragma unroll
         for (int w = 0; w < 16; ++w) {
-          const float f0 = __uint_as_float(v[2 * w]), f1 = __uint_as_float(v[2 * w + 1]);
+          const float2 f = make_float2(__uint_as_float(v[2 * w]), __uint_as_float(v[2 * w + 1]));
           if (EPI == EPI_DGELU) {
             const uint32_t hw = (w & 3) == 0 ? hpre[w >> 2].x : (w & 3) == 1 ? hpre[w >> 2].y
                               : (w & 3) == 2 ? hpre[w >> 2].z : hpre[w >> 2].w;
-            const float2 hv = unpack_bf16x2(hw);
-            o[w] = pack_bf16x2(f0 * gelu_grad_f(hv.x), f1 * gelu_grad_f(hv.y));
+            const float2 r2 = f2mul(f, gelu_grad2(unpack_bf16x2(hw)));
+            o[w] = pack_bf16x2(r2.x, r2.y);
           } else {
-            o[w] = pack_bf16x2(f0, f1);
-            if (EPI == EPI_GELU) g[w] = pack_bf16x2(gelu_f(f0), gelu_f(f1));
+            o[w] = pack_bf16x2(f.x, f.y);
+            if (EPI == EPI_GELU) {
+              const float2 gg = gelu2(f);
+              g[w] = pack_bf16x2(gg.x, gg.y);
+            }
           }
         }
         const int bi = chunk_ctr & 1;
@@ -540,6 +554,7 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensor
                     const CUtensorMap& tx, const Params& p, cudaStream_t s) {
   static bool attr = false;
   auto k = gemm2_kernel<A_MN, B_MN, EPI>;
+  constexpr int SMEM2_BYTES = smem2_bytes(EPI);
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES);
     if (e != cudaSuccess) return e;
@@ -549,7 +564,7 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensor
   if (p.total_tiles < clusters) clusters = p.total_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(NUM_THREADS2);
   cfg.dynamicSmemBytes = SMEM2_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];

@@ -37,8 +37,10 @@ def main():
     dW2 = torch.empty_like(W2)
     cases = {
         "F6 X.W1^T+gelu": (X, W1, Hp, 0, 0, 1, A),
+        "F6-shape plain": (X, W1, Hp, 0, 0, 0, None),
         "F7 A.W2^T": (A, W2, Y, 0, 0, 0, None),
         "B4 dY.W2*gelu'": (Y, W2, A, 0, 1, 2, Hp),
+        "B4-shape plain": (Y, W2, A, 0, 1, 0, None),
         "B5 dH.W1": (A, W1, X, 0, 1, 0, None),
         "B6 dY^T.A": (Y, A, dW2, 1, 1, 0, None),
         "B6 dH^T.X": (A, X, dW1, 1, 1, 0, None),
