@@ -311,6 +311,22 @@ def main():
                 "algorithmic_flop_per_launch": gemm_flops_step / 6.0,
                 "ms_per_launch": gemm_launch_ms, "share_of_step": gemm_ms / ms}
     per_class = {k: v / args.steps for k, v in st["kernel_ms"].items()}
+    # HBM-bound steps: algorithmic bytes per step / measured time; slices of the
+    # slot space this rank dispatches: DTD -> 1 of G_t, vanilla / G_t = 1 -> all
+    C = L["capacity"]
+    slot_rows = E * C // (gt if (dtd and gt > 1) else 1)
+    kept_group = kept_local
+    row = H * 2
+    hbm_bytes = {"dispatch": 2 * slot_rows * row,                       # read x row, write slot row
+                 "combine": 2 * T * row,                                # read O row, write y row
+                 "combine_bwd": 2 * T * row + slot_rows * row}          # read dy + O, write dO
+    hbm = {}
+    for k, b in hbm_bytes.items():
+        t_ms = per_class.get(k, 0.0)
+        if t_ms > 0:
+            gbs = b / (t_ms / 1e3) / 1e9
+            hbm[k] = {"bytes": b, "ms": t_ms, "GB/s": gbs, "frac": gbs / peaks["hbm_gbs"]}
+    del kept_group
 
     # ---- e2e through the public API with host buffers (pinned). Every step copies its
     # inputs host->device and its results device->host inside the timed region; the
@@ -393,7 +409,7 @@ def main():
                           "capacity_factor": 1.0, "g_tensor": gt, "g_expert": gep,
                           "dtd": bool(dtd and gt > 1), "token_groups": S,
                           "l2": "no flush: >1 GB expert weights + activations per step exceed 126 MB L2"},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline, "hbm_steps": hbm, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(round(launches_per_step * args.steps)),
                "launches_per_step": launches_per_step, "clocks": clk,
                "kernel_ms_per_step": per_class,

@@ -142,7 +142,8 @@ moe_status moe_plan_layout(const moe_config* cfg, int world, int rank, moe_layou
 /* Sizes of the caller-allocated buffers: saved (one forward's stash for its
  * backward: routing record, expert inputs X, Hpre, A = gelu(Hpre), combine
  * source O) and scratch (transient; may be shared by consecutive calls on one
- * stream). Both must be 256-byte aligned device memory. */
+ * stream). Both must be 256-byte aligned device memory. The saved blob keeps
+ * G = gelu'(Hpre) rather than Hpre itself (the backward only needs gelu'). */
 moe_status moe_plan_bytes(const moe_config* cfg, int world, int rank,
                           size_t* saved_bytes, size_t* scratch_bytes);
 
@@ -210,8 +211,9 @@ const char* moe_last_error_detail(void);
  *   B: b_mn == 0 -> [batch][N][K] (K-major);  b_mn == 1 -> [batch][K][N]
  *   D: [batch][M][N].  M, K >= 1; N % 64 == 0; M, K, N multiples of 8.
  *   epilogue 0: D = bf16(acc)
- *   epilogue 1: D = bf16(acc) (Hpre), aux = bf16(gelu_tanh(acc)) [batch][M][N]
- *   epilogue 2: D = bf16(acc * gelu_tanh'(aux)), aux = Hpre bf16 [batch][M][N] (read)
+ *   epilogue 1: D = bf16(gelu_tanh'(acc)), aux = bf16(gelu_tanh(acc)) [batch][M][N]
+ *               (the forward FFN GEMM: A for the second GEMM, G = gelu'(Hpre) for B4)
+ *   epilogue 2: D = bf16(acc * aux), aux = G bf16 [batch][M][N] (read) (dGeLU)
  *   impl 0: tcgen05 CTA-pair kernel (cta_group::2, the product path);
  *   impl 2: tcgen05 single-CTA kernel; impl 1: plain SIMT reference kernel
  *   (bring-up cross-check only; never used by moe_forward/backward). */

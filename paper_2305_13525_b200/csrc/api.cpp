@@ -606,12 +606,12 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
     }
   }
 
-  // F6 GEMM1 + GeLU, F7 GEMM2
-  void* Hpre = at<uint8_t>(saved, sv.Hpre);
+  // F6 GEMM1 + GeLU (stores A = gelu(Hpre) and G = gelu'(Hpre)), F7 GEMM2
+  void* G = at<uint8_t>(saved, sv.G);
   void* A = at<uint8_t>(saved, sv.A);
   void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
   void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
-  GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, Hpre, EPI_GELU, A};
+  GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
   TRY(gemm(c, g1, st));
   GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
   TRY(gemm(c, g2, st));
@@ -677,7 +677,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   const float* logits = at<float>(saved, sv.logits);
   const int32_t* count = at<int32_t>(saved, sv.count);
   const void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
-  const void* Hpre = at<uint8_t>(saved, sv.Hpre);
+  const void* G = at<uint8_t>(saved, sv.G);
   const void* A = at<uint8_t>(saved, sv.A);
   const void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
   float* dp = at<float>(c->scratch, sc.dp);
@@ -707,8 +707,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       if (d.dtd) TRY(ag_expert(c, 1, dY, st));
     }
   }
-  // B4 dHpre = (dY W2) * gelu'(Hpre); B5 dXpart = dHpre W1; B6 dW2 = dY^T A, dW1 = dHpre^T X
-  GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(Hpre)};
+  // B4 dHpre = (dY W2) * G; B5 dXpart = dHpre W1; B6 dW2 = dY^T A, dW1 = dHpre^T X
+  GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(G)};
   TRY(gemm(c, g4, st));
   GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
   TRY(gemm(c, g5, st));

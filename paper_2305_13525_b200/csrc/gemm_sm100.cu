@@ -17,8 +17,9 @@
 //  * operands may be K-major or MN-major (instruction-descriptor bits), which
 //    covers the forward (X W1^T, A W2^T), the data-gradient (dY W2, dH W1)
 //    and the weight-gradient (dY^T A, dH^T X) GEMMs without transposes;
-//  * epilogues: plain store; GeLU (stores Hpre and A = gelu(Hpre)); dGeLU
-//    (multiplies by gelu'(Hpre) read from global).
+//  * epilogues: plain store; GeLU (stores G = gelu'(Hpre) for the backward and
+//    A = gelu(Hpre)); dGeLU (multiplies by G read from global) — the backward's
+//    dGeLU becomes one multiply and Hpre itself is never stored.
 //  * no split-K: a row's result never depends on its position, which DTD's
 //    bitwise-equality property relies on.
 #include <cuda.h>
@@ -216,8 +217,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int w = 0; w < 4; ++w) {
                 float2 hv = unpack_bf16x2(hw[w]);
-                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]) * gelu_grad_f(hv.x),
-                                   __uint_as_float(v[q * 8 + 2 * w + 1]) * gelu_grad_f(hv.y));
+                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]) * hv.x,
+                                   __uint_as_float(v[q * 8 + 2 * w + 1]) * hv.y);
               }
               st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
             }
@@ -226,9 +227,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int q = 0; q < 4; ++q) {
               uint32_t o[4];
 #pragma unroll
-              for (int w = 0; w < 4; ++w)
-                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]),
-                                   __uint_as_float(v[q * 8 + 2 * w + 1]));
+              for (int w = 0; w < 4; ++w) {
+                const float f0 = __uint_as_float(v[q * 8 + 2 * w]), f1 = __uint_as_float(v[q * 8 + 2 * w + 1]);
+                o[w] = EPI == EPI_GELU ? pack_bf16x2(gelu_grad_f(f0), gelu_grad_f(f1)) : pack_bf16x2(f0, f1);
+              }
               st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
             }
             if (EPI == EPI_GELU) {
@@ -453,16 +455,19 @@ __global__ void __launch_bounds__(NUM_THREADS2, 1)
         for (int w = 0; w < 16; ++w) {
           const float2 f = make_float2(__uint_as_float(v[2 * w]), __uint_as_float(v[2 * w + 1]));
           if (EPI == EPI_DGELU) {
+            // aux holds gelu'(Hpre) (stored by the forward GeLU epilogue)
             const uint32_t hw = (w & 3) == 0 ? hpre[w >> 2].x : (w & 3) == 1 ? hpre[w >> 2].y
                               : (w & 3) == 2 ? hpre[w >> 2].z : hpre[w >> 2].w;
-            const float2 r2 = f2mul(f, gelu_grad2(unpack_bf16x2(hw)));
+            const float2 r2 = f2mul(f, unpack_bf16x2(hw));
             o[w] = pack_bf16x2(r2.x, r2.y);
+          } else if (EPI == EPI_GELU) {
+            // D = gelu'(acc) (for the backward), aux = gelu(acc) (the FFN activation)
+            const float2 gp = gelu_grad2(f);
+            const float2 gg = gelu2(f);
+            o[w] = pack_bf16x2(gp.x, gp.y);
+            g[w] = pack_bf16x2(gg.x, gg.y);
           } else {
             o[w] = pack_bf16x2(f.x, f.y);
-            if (EPI == EPI_GELU) {
-              const float2 gg = gelu2(f);
-              g[w] = pack_bf16x2(gg.x, gg.y);
-            }
           }
         }
         const int bi = chunk_ctr & 1;
@@ -659,8 +664,8 @@ __global__ void gemm_ref_kernel(GemmArgs a) {
     const size_t o = ((size_t)b * a.M + m) * a.N + n;
     bf16* D = static_cast<bf16*>(a.D);
     bf16* X = static_cast<bf16*>(a.aux);
-    if (a.epilogue == EPI_DGELU) acc *= gelu_grad_f(__bfloat162float(X[o]));
-    D[o] = __float2bfloat16_rn(acc);
+    if (a.epilogue == EPI_DGELU) acc *= __bfloat162float(X[o]);
+    D[o] = __float2bfloat16_rn(a.epilogue == EPI_GELU ? gelu_grad_f(acc) : acc);
     if (a.epilogue == EPI_GELU) X[o] = __float2bfloat16_rn(gelu_f(acc));
   }
 }

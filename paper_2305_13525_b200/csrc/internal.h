@@ -18,7 +18,7 @@ struct GemmArgs {
   int b_mn;  // 0: B [b][N][K]; 1: B [b][K][N]
   void* D;   // [b][M][N]
   int epilogue;
-  void* aux;  // EPI_GELU: out [b][M][N]; EPI_DGELU: in (Hpre) [b][M][N]
+  void* aux;  // EPI_GELU: out A = gelu(acc) [b][M][N] (D = gelu'(acc)); EPI_DGELU: in G [b][M][N] (D = acc*G)
   int variant = 0;  // 0: CTA-pair kernel (cta_group::2, product path); 1: single-CTA kernel
 };
 

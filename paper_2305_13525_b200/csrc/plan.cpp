@@ -83,7 +83,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sv->tok_of = s.take((size_t)d.E * d.C * 4);
   // peer mode keeps X and O in the library's ring windows instead of the saved blob
   sv->X = d.peer ? 0 : s.take(expert_space);
-  sv->Hpre = s.take(ffn_space);
+  sv->G = s.take(ffn_space);
   sv->A = s.take(ffn_space);
   sv->O = d.peer ? 0 : s.take(slot_space);
   sv->total = s.off;

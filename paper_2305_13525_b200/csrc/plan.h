@@ -29,7 +29,7 @@ struct Dims {
 moe_status make_dims(const moe_config* cfg, int world, int rank, Dims* d, std::string* why);
 
 struct SavedLayout {
-  size_t logits, expert, slot, prob, gap, count, load, ties, tok_of, X, Hpre, A, O, total;
+  size_t logits, expert, slot, prob, gap, count, load, ties, tok_of, X, G, A, O, total;  // G = gelu'(Hpre)
 };
 struct ScratchLayout {
   // forward
