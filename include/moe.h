@@ -62,6 +62,15 @@ typedef enum {
 #define MOE_F_TIMING 4u           /* record CUDA events around every kernel class (moe_stats) */
 #define MOE_F_NCCL_EXCHANGE 8u    /* EP exchange via NCCL send/recv + all-gather (baseline)
                                      instead of the peer-memory copy kernel (default)       */
+#define MOE_F_CHECKPOINT 16u      /* activation checkpointing: the
+                                     forward keeps the routing record and the outputs of its
+                                     collectives (X, O: the CAC stash) but
+                                     not G/A; moe_forward_replay re-materializes them before
+                                     moe_backward                                           */
+#define MOE_F_CAC 32u             /* with MOE_F_CHECKPOINT: the replay reuses the stash and
+                                     issues no collectives (Communication-aware Activation
+                                     Checkpointing); without it the replay
+                                     re-runs the forward's collectives (plain checkpointing) */
 
 /* Layer configuration. Identical on every rank of the job.
  * Constraints (checked, MOE_ERR_SHAPE otherwise):
@@ -106,7 +115,7 @@ enum { MOE_COLL_A2A = 0, MOE_COLL_ALLGATHER = 1, MOE_COLL_REDUCESCATTER = 2,
  * all-reduce: 2(s-1)/s x the buffer (s = group size). */
 typedef struct {
   int32_t kind;            /* MOE_COLL_*                                               */
-  int32_t pass;            /* 0 = forward, 1 = backward                                */
+  int32_t pass;            /* 0 = forward, 1 = backward, 2 = checkpoint replay          */
   int32_t step;            /* SURVEY §8(a) step id: 4,5,8,9,10 (F) / 2,3,7,8,9 (B)      */
   int32_t group_size;      /* s                                                        */
   int64_t buffer_bytes;    /* full buffer (a2a: send buffer incl. self chunk)          */
@@ -132,6 +141,7 @@ typedef struct {
   int32_t nccl_async_error;/* ncclCommGetAsyncError of the last check (0 = none)      */
   int64_t kernel_launches[MOE_K_CLASSES]; /* CUDA kernels this library launched, per class */
   double kernel_ms[MOE_K_CLASSES];        /* MOE_F_TIMING: summed CUDA-event time per class */
+  int64_t replay_calls;                   /* collectives issued by moe_forward_replay       */
 } moe_stats;
 
 /* ---------------- host-only planning (no GPU, no ctx) ---------------- */
@@ -187,6 +197,16 @@ moe_status moe_forward(moe_ctx* ctx, const void* x, const float* wg, const void*
 moe_status moe_backward(moe_ctx* ctx, const void* dy, const void* saved, const void* x,
                         const float* wg, const void* w1, const void* w2, void* dx,
                         float* dwg, void* dw1, void* dw2, void* stream);
+
+/* Checkpoint replay (MOE_F_CHECKPOINT only): re-materializes G = gelu'(Hpre)
+ * and A = gelu(Hpre) of a checkpointed forward into the ctx scratch, ahead of
+ * moe_backward on the same saved blob. With MOE_F_CAC the replay runs GEMM1 on
+ * the stashed expert inputs X and issues no collective; otherwise it re-runs the
+ * forward (gate, dispatch, exchanges, GEMMs, TP reduction) including every
+ * collective, as plain activation checkpointing does. Arguments as moe_forward.
+ * The scratch holds one replay at a time: replay, then backward, per layer. */
+moe_status moe_forward_replay(moe_ctx* ctx, const void* saved, const void* x, const float* wg,
+                              const void* w1, const void* w2, void* stream);
 
 /* Copies the routing record of a saved blob (device -> device, async).
  * expert/slot int32 [T] (slot -1 = dropped), prob/gap fp32 [T],

@@ -5,6 +5,6 @@ expert FFN, weighted combine — behind the C ABI of include/moe.h.
 The CUDA library (libmoe.so) is loaded lazily by `binding.lib()`; there is no
 CPU fallback.
 """
-from .binding import (MOE_F_FORCED_ROUTING, MOE_F_NCCL_EXCHANGE, MOE_F_STATS, MOE_F_TIMING, MoEConfig, MoEError, MoEFunction,  # noqa: F401
+from .binding import (MOE_F_CAC, MOE_F_CHECKPOINT, MOE_F_FORCED_ROUTING, MOE_F_NCCL_EXCHANGE, MOE_F_STATS, MOE_F_TIMING, MoEConfig, MoEError, MoEFunction,  # noqa: F401
                       MoELayer, lib, moe_gemm_bf16, moe_get_unique_id, moe_plan_bytes,
                       moe_plan_collectives, moe_plan_layout)

@@ -19,6 +19,8 @@ MOE_F_STATS = 1
 MOE_F_FORCED_ROUTING = 2
 MOE_F_TIMING = 4
 MOE_F_NCCL_EXCHANGE = 8
+MOE_F_CHECKPOINT = 16
+MOE_F_CAC = 32
 KERNEL_CLASSES = ("route", "dispatch", "gemm", "combine", "combine_bwd", "gate_bwd", "comm")
 COLL_NAMES = ("a2a", "allgather", "reducescatter", "allreduce")
 
@@ -57,11 +59,12 @@ class _Stats(ctypes.Structure):
                 ("forward_calls", ctypes.c_int64), ("backward_calls", ctypes.c_int64),
                 ("dropped_tokens", ctypes.c_int64), ("tie_tokens", ctypes.c_int64),
                 ("nccl_async_error", ctypes.c_int32),
-                ("kernel_launches", ctypes.c_int64 * 7), ("kernel_ms", ctypes.c_double * 7)]
+                ("kernel_launches", ctypes.c_int64 * 7), ("kernel_ms", ctypes.c_double * 7),
+                ("replay_calls", ctypes.c_int64)]
 
 
 EXPORTS = ("moe_plan_layout", "moe_plan_bytes", "moe_plan_collectives", "moe_get_unique_id",
-           "moe_create", "moe_forward", "moe_backward", "moe_routing", "moe_stats_get",
+           "moe_create", "moe_forward", "moe_backward", "moe_forward_replay", "moe_routing", "moe_stats_get",
            "moe_stats_reset", "moe_destroy", "moe_status_string", "moe_last_error_detail",
            "moe_gemm_bf16")
 
@@ -86,6 +89,7 @@ def lib() -> ctypes.CDLL:
     L.moe_create.argtypes = [cfgp, ctypes.c_char_p, I, I, P, SZ, ctypes.POINTER(P)]
     L.moe_forward.argtypes = [P, P, P, P, P, P, P, P, P]
     L.moe_backward.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P]
+    L.moe_forward_replay.argtypes = [P, P, P, P, P, P, P]
     L.moe_routing.argtypes = [P, P, P, P, P, P, P, P]
     L.moe_stats_get.argtypes = [P, ctypes.POINTER(_Stats)]
     L.moe_stats_reset.argtypes = [P]
@@ -148,7 +152,7 @@ def moe_plan_collectives(cfg: MoEConfig, world: int = 1, rank: int = 0) -> list[
     _check(L.moe_plan_collectives(ctypes.byref(cfg.c()), world, rank, None, 0, ctypes.byref(n)))
     arr = (_Collective * max(n.value, 1))()
     _check(L.moe_plan_collectives(ctypes.byref(cfg.c()), world, rank, arr, n.value, ctypes.byref(n)))
-    return [{"kind": COLL_NAMES[a.kind], "pass": ("forward", "backward")[a.pass_], "step": a.step,
+    return [{"kind": COLL_NAMES[a.kind], "pass": ("forward", "backward", "replay")[a.pass_], "step": a.step,
              "group_size": a.group_size, "buffer_bytes": a.buffer_bytes, "wire_bytes": a.wire_bytes}
             for a in arr[:n.value]]
 
@@ -221,6 +225,10 @@ class MoELayer:
                                   _ptr(w2), _ptr(dx), _ptr(dwg), _ptr(dw1), _ptr(dw2), _stream(stream)))
         return dx, dwg, dw1, dw2
 
+    def moe_forward_replay(self, saved, x, wg, w1, w2, stream=None):
+        _check(lib().moe_forward_replay(self.ctx, _ptr(saved), _ptr(x), _ptr(wg), _ptr(w1), _ptr(w2),
+                                        _stream(stream)))
+
     def moe_routing(self, saved, stream=None) -> dict:
         T, E = self.cfg.tokens, self.cfg.experts
         dev = self.device
@@ -242,7 +250,8 @@ class MoELayer:
                 "dropped_tokens": s.dropped_tokens, "tie_tokens": s.tie_tokens,
                 "nccl_async_error": s.nccl_async_error,
                 "kernel_launches": dict(zip(KERNEL_CLASSES, list(s.kernel_launches))),
-                "kernel_ms": dict(zip(KERNEL_CLASSES, list(s.kernel_ms)))}
+                "kernel_ms": dict(zip(KERNEL_CLASSES, list(s.kernel_ms))),
+                "replay_calls": s.replay_calls}
 
     def moe_stats_reset(self):
         _check(lib().moe_stats_reset(self.ctx))

@@ -49,6 +49,7 @@ struct moe_ctx {
   uint64_t gen = 0;
   uint64_t ring_gen[2] = {0, 0};
   std::unordered_map<const void*, std::pair<int, uint64_t>> saved_slot;  // saved -> (ring slot, gen)
+  const void* replayed = nullptr;  // MOE_F_CHECKPOINT: saved blob whose G/A sit in scratch
   const void* last_saved = nullptr;
   cudaStream_t last_stream = nullptr;
   // MOE_F_TIMING: event pairs per kernel class, resolved in moe_stats_get
@@ -138,7 +139,9 @@ SlotSpace slot_space(const Dims& d) {
 void ledger(moe_ctx* c, int kind, int pass, int64_t wire) {
   c->stats.calls[kind] += 1;
   c->stats.wire_bytes[kind] += wire;
-  if (pass == 0) c->stats.forward_calls += 1; else c->stats.backward_calls += 1;
+  if (pass == 0) c->stats.forward_calls += 1;
+  else if (pass == 1) c->stats.backward_calls += 1;
+  else c->stats.replay_calls += 1;
 }
 
 // ---- EP exchange between slot space S and expert space X (F4/F9/B2/B8) ----
@@ -407,6 +410,85 @@ moe_status exchange(moe_ctx* c, bool dispatch, int pass, const void* src, int wi
 
 }  // namespace
 
+// F3-F11 of one forward on an already-routed saved blob. pass 0: the forward
+// (y written); pass 2: a plain-checkpointing replay (y == nullptr, every collective
+// re-issued and counted as replay). rslot: ring slot of the peer windows.
+moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w2, void* y,
+                        void* saved, cudaStream_t st, int pass, int rslot) {
+  const Dims& d = c->d;
+  const SavedLayout& sv = c->sv;
+  const ScratchLayout& sc = c->sc;
+  const SlotSpace ss = slot_space(d);
+  const bool solo = d.world == 1;
+  const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
+  // F3 dispatch (DTD: only this rank's slot slice), F4 a2a, F5 all-gather
+  void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
+  const int32_t* tok_of = at<int32_t>(saved, sv.tok_of);
+  const int32_t* count = at<int32_t>(saved, sv.count);
+  void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
+  if (d.peer) {
+    // fused: rows go straight from x into the peers' expert-space windows
+    {
+      Scope sc_(c, MOE_K_DISPATCH, st, 1);
+      CUDA_TRY(c, dispatch_peer(x, tok_of, count, ss, lo, hi, peer_dst(c, moe_ctx::W_X0 + rslot), st));
+    }
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(publish(c, true, pass, st));
+  } else {
+    Scope sc_(c, MOE_K_DISPATCH, st, 1);
+    CUDA_TRY(c, dispatch(x, tok_of, count, ss, lo, hi, D, st));
+  }
+  if (!solo && !d.peer) {
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    {
+      TRY(ep_exchange(c, 0, pass, D, X, lo, hi, st));
+      if (d.dtd) TRY(ag_expert(c, pass, X, st));
+    }
+  }
+  if (d.peer && d.ckpt) {  // CAC stash of the first collective's output
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.X), X, (size_t)d.El * d.R * d.H * 2,
+                                cudaMemcpyDeviceToDevice, st));
+  }
+
+  // F6 GEMM1 + GeLU (stores A = gelu(Hpre) and G = gelu'(Hpre)), F7 GEMM2
+  void* G = d.ckpt ? at<uint8_t>(c->scratch, sc.Grec) : at<uint8_t>(saved, sv.G);
+  void* A = d.ckpt ? at<uint8_t>(c->scratch, sc.Arec) : at<uint8_t>(saved, sv.A);
+  void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
+  void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
+  GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
+  TRY(gemm(c, g1, st));
+  GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+  TRY(gemm(c, g2, st));
+
+  // F8 TP reduce, F9 a2a back, F10 all-gather
+  if (!solo) {
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    if (d.Gt > 1) {
+      if (d.dtd) TRY(rs_expert(c, pass, Y, st));
+      else TRY(ar_expert(c, pass, Y, st));
+    }
+    if (d.peer) {
+      TRY(exchange(c, false, pass, Y, moe_ctx::W_O0 + rslot, st));
+    } else {
+      TRY(ep_exchange(c, 1, pass, O, Y, lo, hi, st));
+      if (d.dtd) TRY(ag_slot(c, pass, O, st));
+    }
+    if (d.peer && d.ckpt) {  // CAC stash of the second collective's output
+      CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.O), O, (size_t)d.E * d.C * d.H * 2,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+  }
+
+  // F11 combine (not in a checkpoint replay: the layer output is not needed again)
+  if (y) {
+    Scope sc_(c, MOE_K_COMBINE, st, 1);
+    CUDA_TRY(c, combine(O, at<int32_t>(saved, sv.expert), at<int32_t>(saved, sv.slot),
+                        at<float>(saved, sv.prob), ss, d.T, y, st));
+  }
+  return MOE_OK;
+}
+
 extern "C" {
 
 const char* moe_status_string(moe_status s) {
@@ -556,9 +638,6 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const SavedLayout& sv = c->sv;
   const ScratchLayout& sc = c->sc;
-  const SlotSpace ss = slot_space(d);
-  const bool solo = d.world == 1;
-  const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
 
   // F1 + F2: gate and capacity slots
   RouteArgs ra;
@@ -582,60 +661,8 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   // ring slot of the peer windows used by this forward
   const int rslot = (int)(c->gen & 1);
   const uint64_t mygen = ++c->gen;
-
-  // F3 dispatch (DTD: only this rank's slot slice), F4 a2a, F5 all-gather
-  void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
-  void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
-  if (d.peer) {
-    // fused: rows go straight from x into the peers' expert-space windows
-    {
-      Scope sc_(c, MOE_K_DISPATCH, st, 1);
-      CUDA_TRY(c, dispatch_peer(x, ra.tok_of, ra.count, ss, lo, hi, peer_dst(c, moe_ctx::W_X0 + rslot), st));
-    }
-    Scope sc_(c, MOE_K_COMM, st, 0);
-    TRY(publish(c, true, 0, st));
-  } else {
-    Scope sc_(c, MOE_K_DISPATCH, st, 1);
-    CUDA_TRY(c, dispatch(x, ra.tok_of, ra.count, ss, lo, hi, D, st));
-  }
-  if (!solo && !d.peer) {
-    Scope sc_(c, MOE_K_COMM, st, 0);
-    {
-      TRY(ep_exchange(c, 0, 0, D, X, lo, hi, st));
-      if (d.dtd) TRY(ag_expert(c, 0, X, st));
-    }
-  }
-
-  // F6 GEMM1 + GeLU (stores A = gelu(Hpre) and G = gelu'(Hpre)), F7 GEMM2
-  void* G = at<uint8_t>(saved, sv.G);
-  void* A = at<uint8_t>(saved, sv.A);
-  void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
-  void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
-  GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
-  TRY(gemm(c, g1, st));
-  GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
-  TRY(gemm(c, g2, st));
-
-  // F8 TP reduce, F9 a2a back, F10 all-gather
-  if (!solo) {
-    Scope sc_(c, MOE_K_COMM, st, 0);
-    if (d.Gt > 1) {
-      if (d.dtd) TRY(rs_expert(c, 0, Y, st));
-      else TRY(ar_expert(c, 0, Y, st));
-    }
-    if (d.peer) {
-      TRY(exchange(c, false, 0, Y, moe_ctx::W_O0 + rslot, st));
-    } else {
-      TRY(ep_exchange(c, 1, 0, O, Y, lo, hi, st));
-      if (d.dtd) TRY(ag_slot(c, 0, O, st));
-    }
-  }
-
-  // F11 combine
-  {
-    Scope sc_(c, MOE_K_COMBINE, st, 1);
-    CUDA_TRY(c, combine(O, ra.expert, ra.slot, ra.prob, ss, d.T, y, st));
-  }
+  TRY(forward_core(c, x, w1, w2, y, saved, st, 0, rslot));
+  if (d.ckpt && c->replayed == saved) c->replayed = nullptr;  // G/A in scratch are stale now
   c->saved_written.insert(saved);
   c->saved_slot[saved] = {rslot, mygen};
   c->ring_gen[rslot] = mygen;
@@ -654,7 +681,9 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   if (!c->saved_written.count(saved))
     return fail(MOE_ERR_STATE, "saved blob was not written by moe_forward on this ctx");
   int rslot = 0;
-  if (c->d.peer) {
+  if (c->d.ckpt && c->replayed != saved)
+    return fail(MOE_ERR_STATE, "checkpointed forward: call moe_forward_replay on this saved blob first");
+  if (c->d.peer && !c->d.ckpt) {
     const auto it = c->saved_slot.find(saved);
     if (it == c->saved_slot.end() || c->ring_gen[it->second.first] != it->second.second)
       return fail(MOE_ERR_STATE, "saved blob's peer window was reused: more than 1 newer forward ran "
@@ -676,10 +705,11 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   const float* prob = at<float>(saved, sv.prob);
   const float* logits = at<float>(saved, sv.logits);
   const int32_t* count = at<int32_t>(saved, sv.count);
-  const void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
-  const void* G = at<uint8_t>(saved, sv.G);
-  const void* A = at<uint8_t>(saved, sv.A);
-  const void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
+  const bool win_xo = d.peer && !d.ckpt;  // X/O in the ring windows (else saved / CAC stash)
+  const void* X = win_xo ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
+  const void* G = d.ckpt ? at<uint8_t>(c->scratch, sc.Grec) : at<uint8_t>(saved, sv.G);
+  const void* A = d.ckpt ? at<uint8_t>(c->scratch, sc.Arec) : at<uint8_t>(saved, sv.A);
+  const void* O = win_xo ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
   float* dp = at<float>(c->scratch, sc.dp);
   void* dY = d.peer ? c->win[moe_ctx::W_DY] : at<uint8_t>(c->scratch, sc.dY);
   void* dO = at<uint8_t>(c->scratch, sc.dO);
@@ -737,6 +767,38 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
                          at<float>(c->scratch, sc.dl), at<float>(c->scratch, sc.dwgp), sc.nsplit,
                          at<uint8_t>(c->scratch, sc.wpk), st));
   }
+  c->last_stream = st;
+  return MOE_OK;
+}
+
+moe_status moe_forward_replay(moe_ctx* c, const void* saved, const void* x, const float* wg,
+                              const void* w1, const void* w2, void* stream) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  if (c->poisoned) return fail(MOE_ERR_STATE, "ctx poisoned by an earlier CUDA/NCCL failure");
+  if (!c->d.ckpt) return fail(MOE_ERR_STATE, "moe_forward_replay needs MOE_F_CHECKPOINT");
+  if (!saved || !x || !wg || !w1 || !w2) return fail(MOE_ERR_ARG, "null tensor pointer");
+  if (!c->saved_written.count(saved))
+    return fail(MOE_ERR_STATE, "saved blob was not written by moe_forward on this ctx");
+  const Dims& d = c->d;
+  const SavedLayout& sv = c->sv;
+  const ScratchLayout& sc = c->sc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* sv_mut = const_cast<void*>(saved);
+  if (d.cac) {
+    // CAC: the stashed output of the first collective (X) feeds
+    // GEMM1 directly; no gate, no dispatch, no collective is re-issued.
+    GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, at<uint8_t>(sv_mut, sv.X), 0, w1, 0,
+                at<uint8_t>(c->scratch, sc.Grec), EPI_GELU, at<uint8_t>(c->scratch, sc.Arec)};
+    TRY(gemm(c, g1, st));
+  } else {
+    // plain activation checkpointing: the whole forward again (routing record reused:
+    // it is deterministic and needs no communication), every collective re-issued
+    const int rslot = (int)(c->gen & 1);
+    ++c->gen;
+    TRY(forward_core(c, x, w1, w2, nullptr, sv_mut, st, 2, rslot));
+  }
+  (void)wg;
+  c->replayed = saved;
   c->last_stream = st;
   return MOE_OK;
 }

@@ -26,7 +26,8 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   const int tp_ep = c->g_tensor * c->g_expert;
   if (world % tp_ep) { *why = "world % (g_tensor * g_expert) != 0"; return MOE_ERR_SHAPE; }
   if (c->tokens > (int64_t)1 << 30) { *why = "tokens must be < 2^30"; return MOE_ERR_SHAPE; }
-  if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING | MOE_F_NCCL_EXCHANGE)) { *why = "unknown flag bits"; return MOE_ERR_ARG; }
+  if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING | MOE_F_NCCL_EXCHANGE |
+                   MOE_F_CHECKPOINT | MOE_F_CAC)) { *why = "unknown flag bits"; return MOE_ERR_ARG; }
   d->T = c->tokens;
   d->H = c->hidden;
   d->F = c->ffn;
@@ -52,6 +53,9 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->dtd = c->dtd != 0 && d->Gt > 1;
   d->forced = (c->flags & MOE_F_FORCED_ROUTING) != 0;
   d->peer = world > 1 && (c->flags & MOE_F_NCCL_EXCHANGE) == 0;
+  d->ckpt = (c->flags & MOE_F_CHECKPOINT) != 0;
+  d->cac = d->ckpt && (c->flags & MOE_F_CAC) != 0;
+  if ((c->flags & MOE_F_CAC) && !d->ckpt) { *why = "MOE_F_CAC needs MOE_F_CHECKPOINT"; return MOE_ERR_ARG; }
   if (d->R > (int64_t)1 << 30) { *why = "rows per expert too large"; return MOE_ERR_SHAPE; }
   return MOE_OK;
 }
@@ -81,11 +85,13 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sv->load = s.take((size_t)d.E * 4);
   sv->ties = s.take(4);
   sv->tok_of = s.take((size_t)d.E * d.C * 4);
-  // peer mode keeps X and O in the library's ring windows instead of the saved blob
-  sv->X = d.peer ? 0 : s.take(expert_space);
-  sv->G = s.take(ffn_space);
-  sv->A = s.take(ffn_space);
-  sv->O = d.peer ? 0 : s.take(slot_space);
+  // peer mode keeps X and O in the library's ring windows instead of the saved blob,
+  // except under checkpointing, where they are the CAC stash; checkpointing keeps G/A
+  // out of the saved blob (the replay re-materializes them in scratch)
+  sv->X = (d.peer && !d.ckpt) ? 0 : s.take(expert_space);
+  sv->G = d.ckpt ? 0 : s.take(ffn_space);
+  sv->A = d.ckpt ? 0 : s.take(ffn_space);
+  sv->O = (d.peer && !d.ckpt) ? 0 : s.take(slot_space);
   sv->total = s.off;
 
   const bool solo = d.world == 1;  // slot space == expert space, no communication
@@ -109,7 +115,16 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dH = b.take(ffn_space);
   sc->dXp = b.take(expert_space);
   sc->dS = solo ? sc->dXp : (d.peer ? 0 : b.take(slot_space));  // peer mode: window WdS
-  sc->total = f.off > b.off ? f.off : b.off;
+  size_t top = f.off > b.off ? f.off : b.off;
+  sc->Grec = sc->Arec = 0;
+  if (d.ckpt) {
+    Bump r;
+    r.off = top;
+    sc->Grec = r.take(ffn_space);
+    sc->Arec = r.take(ffn_space);
+    top = r.off;
+  }
+  sc->total = top;
 }
 
 std::vector<moe_collective> make_schedule(const Dims& d) {
@@ -127,11 +142,14 @@ std::vector<moe_collective> make_schedule(const Dims& d) {
   const int64_t xe = (int64_t)d.El * d.R * d.H * elt;                       // expert-space buffer
   const int64_t O = (int64_t)d.E * d.C * d.H * elt;                         // slot-space buffer
   const int64_t g = d.Gt;
-  for (int pass = 0; pass < 2; ++pass) {
+  const int npass = (d.ckpt && !d.cac) ? 3 : 2;  // plain checkpointing replays the forward's collectives
+  for (int pi = 0; pi < npass; ++pi) {
+    const int pass = npass == 3 ? (pi == 0 ? 0 : (pi == 1 ? 2 : 1)) : pi;  // issue order
     // forward: F4 a2a, F5 AG (DTD), [GEMMs], F8 RS/AR, F9 a2a, F10 AG (DTD)
     // backward mirrors it: B2 a2a, B3 AG (DTD), [GEMMs], B7 RS/AR, B8 a2a, B9 AG (DTD)
-    const int s_a2a1 = pass ? 2 : 4, s_ag1 = pass ? 3 : 5, s_red = pass ? 7 : 8;
-    const int s_a2a2 = pass ? 8 : 9, s_ag2 = pass ? 9 : 10;
+    const bool bwd = pass == 1;  // replay (pass 2) repeats the forward steps
+    const int s_a2a1 = bwd ? 2 : 4, s_ag1 = bwd ? 3 : 5, s_red = bwd ? 7 : 8;
+    const int s_a2a2 = bwd ? 8 : 9, s_ag2 = bwd ? 9 : 10;
     if (d.Gep > 1) push(MOE_COLL_A2A, pass, s_a2a1, d.Gep, a2a_buf, a2a_wire);
     if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag1, d.Gt, xe, xe * (g - 1) / g);
     if (d.Gt > 1) {

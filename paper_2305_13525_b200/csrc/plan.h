@@ -23,6 +23,8 @@ struct Dims {
   bool dtd;          // DTD in effect (requested and G_t > 1)
   bool forced;
   bool peer;         // world > 1 and the peer-memory exchange (not MOE_F_NCCL_EXCHANGE)
+  bool ckpt;         // MOE_F_CHECKPOINT
+  bool cac;          // MOE_F_CAC (with ckpt)
 };
 
 // Validates and derives; returns MOE_OK or an error with *why set.
@@ -36,6 +38,8 @@ struct ScratchLayout {
   size_t local_rank, block_hist, D, Ypart;
   // backward
   size_t dp, dl, dwgp, wpk, dO, dY, dH, dXp, dS;
+  // checkpoint mode: G, A re-materialized by the replay (outside both regions)
+  size_t Grec, Arec;
   size_t total;
   bool D_in_saved, Y_in_saved;  // world == 1: D aliases saved.X, Ypart aliases saved.O
   bool dO_is_dY, dXp_is_dS;     // world == 1: slot space == expert space

@@ -25,7 +25,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import moe_oracle as O  # noqa: E402
-from paper_2305_13525_b200 import MOE_F_NCCL_EXCHANGE, MoEConfig, MoELayer, synth  # noqa: E402
+from paper_2305_13525_b200 import (MOE_F_CAC, MOE_F_CHECKPOINT, MOE_F_NCCL_EXCHANGE, MoEConfig,  # noqa: E402
+                                   MoELayer, synth)
 from tests.helpers import REL_L2_BAR, bf16_tensor, rel_l2, tensor_f64  # noqa: E402
 
 
@@ -58,12 +59,13 @@ def main():
     w1_b, w2_b = synth.make_experts(shape)
 
     results = {}
-    for mode in ((True, False), (False, False), (True, True)):  # (dtd, nccl exchange)
-        dtd, nccl = mode
+    # (dtd, extra flags, key): DTD, vanilla, NCCL-exchange baseline, checkpointing with and without CAC
+    modes = ((True, 0, True), (False, 0, False), (True, MOE_F_NCCL_EXCHANGE, "nccl"),
+             (True, MOE_F_CHECKPOINT | MOE_F_CAC, "cac"), (True, MOE_F_CHECKPOINT, "ckpt"))
+    for dtd, extra, key in modes:
         cfg = MoEConfig.from_shape(shape, dtd=dtd)
-        if nccl:
-            cfg = MoEConfig(cfg.tokens, cfg.hidden, cfg.ffn, cfg.experts, cfg.capacity_factor,
-                            cfg.g_tensor, cfg.g_expert, cfg.dtd, cfg.flags | MOE_F_NCCL_EXCHANGE)
+        cfg = MoEConfig(cfg.tokens, cfg.hidden, cfg.ffn, cfg.experts, cfg.capacity_factor,
+                        cfg.g_tensor, cfg.g_expert, cfg.dtd, cfg.flags | extra)
         layer = MoELayer(cfg, world, rank, dev)
         L = layer.layout
         s = L["d"] * a.gep + L["ep"]
@@ -74,11 +76,12 @@ def main():
         w1 = bf16_tensor(w1s)
         w2 = bf16_tensor(w2s)
         y, saved = layer.moe_forward(x, wgt, w1, w2)
+        if extra & MOE_F_CHECKPOINT:
+            layer.moe_forward_replay(saved, x, wgt, w1, w2)
         dx, dwg, dw1, dw2 = layer.moe_backward(dy, saved, x, wgt, w1, w2)
         rt = layer.moe_routing(saved)
         torch.cuda.synchronize()
         st = layer.moe_stats()
-        key = "nccl" if nccl else dtd
         results[key] = {"y": y.clone(), "dx": dx.clone(), "dwg": dwg.clone(), "dw1": dw1.clone(),
                         "dw2": dw2.clone(), "rt": {k: v.cpu().numpy() for k, v in rt.items()},
                         "stats": st, "layout": L, "group": s}
@@ -146,6 +149,16 @@ def main():
             failures.append(f"peer exchange != NCCL exchange (bitwise) for {k}")
     if nc["stats"]["wire_bytes"] != t_["stats"]["wire_bytes"]:
         failures.append(f"ledger differs: peer {t_['stats']['wire_bytes']} nccl {nc['stats']['wire_bytes']}")
+    # ---- checkpointing: replay (with / without CAC) reproduces the run bitwise; CAC's replay
+    # issues no collective, plain checkpointing re-issues the forward's
+    for key in ("cac", "ckpt"):
+        for k in ("y", "dx", "dwg", "dw1", "dw2"):
+            if not torch.equal(results[key][k], t_[k]):
+                failures.append(f"{key} replay != un-checkpointed run (bitwise) for {k}")
+    if results["cac"]["stats"]["replay_calls"] != 0:
+        failures.append(f"CAC replay issued {results['cac']['stats']['replay_calls']} collectives")
+    if results["ckpt"]["stats"]["replay_calls"] != t_["stats"]["forward_calls"]:
+        failures.append("plain checkpoint replay did not repeat the forward's collectives")
     a2a_dtd = t_["stats"]["wire_bytes"]["a2a"]
     a2a_van = v["stats"]["wire_bytes"]["a2a"]
     if a2a_dtd * a.gt != a2a_van:

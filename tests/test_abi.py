@@ -157,3 +157,36 @@ def test_golden_dtd_example():
     assert [c // lay[0]["slot_slice"] for c in range(kv["capacity"])] == [kv["keeper_a1"], kv["keeper_a2"]]
     full = kv["tokens"] * H * 2
     assert full * (gt - 1) // gt == kv["allgather_rx_bytes"]
+
+
+@pytest.mark.parametrize("gt,gep,dtd", [(2, 4, False), (2, 4, True), (1, 8, True), (4, 2, True)])
+def test_cac_cuts_collective_calls_by_one_third(gt, gep, dtd):
+    """SPEC.md:559 / PAPER.md:1181-1188: with activation checkpointing the replay repeats
+    the forward's collectives (fwd + replay + bwd); CAC replays from the stash with none,
+    so calls and bytes drop by exactly 1/3 and the replay moves 0 bytes."""
+    from paper_2305_13525_b200 import MOE_F_CAC, MOE_F_CHECKPOINT
+    base = MoEConfig(16384, 2560, 10240, 32, 1.0, gt, gep, dtd)
+    ck = MoEConfig(16384, 2560, 10240, 32, 1.0, gt, gep, dtd, base.flags | MOE_F_CHECKPOINT)
+    cac = MoEConfig(16384, 2560, 10240, 32, 1.0, gt, gep, dtd, base.flags | MOE_F_CHECKPOINT | MOE_F_CAC)
+    w = gt * gep
+    s0, s1, s2 = (moe_plan_collectives(c, w, 0) for c in (base, ck, cac))
+    assert s2 == s0                                   # CAC: exactly the un-checkpointed schedule
+    replay = [c for c in s1 if c["pass"] == "replay"]
+    assert [c["kind"] for c in replay] == [c["kind"] for c in s0 if c["pass"] == "forward"]
+    assert len(s2) * 3 == len(s1) * 2
+    tot = lambda s: sum(c["wire_bytes"] for c in s)  # noqa: E731
+    assert tot(s2) * 3 == tot(s1) * 2
+    assert [c["pass"] for c in s1][: len(replay) * 2] == ["forward"] * len(replay) + ["replay"] * len(replay)
+
+
+def test_checkpoint_saved_blob_drops_activations():
+    from paper_2305_13525_b200 import MOE_F_CAC, MOE_F_CHECKPOINT
+    base = MoEConfig.from_shape(synth.CONFIGS["1.3b"])
+    ck = MoEConfig(base.tokens, base.hidden, base.ffn, base.experts, 1.0, 1, 1, True,
+                   base.flags | MOE_F_CHECKPOINT | MOE_F_CAC)
+    s0, _ = moe_plan_bytes(base)
+    s1, sc1 = moe_plan_bytes(ck)
+    ffn = 16 * 1024 * 8192 * 2
+    assert s0 - s1 == 2 * ffn           # G and A are re-materialized by the replay
+    with pytest.raises(MoEError):       # CAC without checkpointing is rejected
+        moe_plan_bytes(MoEConfig(base.tokens, base.hidden, base.ffn, base.experts, flags=1 | MOE_F_CAC))

@@ -183,3 +183,30 @@ def test_forward_errors_are_status_codes():
     rt = layer.moe_routing(saved)
     assert (rt["expert"] == 0).all() and torch.allclose(rt["prob"], torch.full_like(rt["prob"], 0.25))
     layer.close()
+
+
+@pytest.mark.parametrize("cac", [True, False])
+def test_checkpoint_replay_bitwise(cac):
+    """Checkpointed forward + replay + backward == plain forward + backward, bitwise."""
+    from paper_2305_13525_b200 import MOE_F_CAC, MOE_F_CHECKPOINT, MoEError
+    shape = synth.LayerShape("ck", 2048, 256, 512, 8)
+    inp = Inputs(shape)
+    x, dy = bf16_tensor(inp.x[0]), bf16_tensor(inp.dy[0])
+    wg = torch.from_numpy(inp.wg).cuda()
+    w1, w2 = bf16_tensor(inp.w1), bf16_tensor(inp.w2)
+    base = MoEConfig.from_shape(shape)
+    outs = []
+    for flags in (base.flags, base.flags | MOE_F_CHECKPOINT | (MOE_F_CAC if cac else 0)):
+        layer = MoELayer(MoEConfig(shape.tokens, shape.hidden, shape.ffn, shape.experts, 1.0, 1, 1, True, flags))
+        y, saved = layer.moe_forward(x, wg, w1, w2)
+        if flags & MOE_F_CHECKPOINT:
+            with pytest.raises(MoEError) as ei:
+                layer.moe_backward(dy, saved, x, wg, w1, w2)
+            assert ei.value.name == "MOE_ERR_STATE"
+            layer.moe_forward_replay(saved, x, wg, w1, w2)
+        g = layer.moe_backward(dy, saved, x, wg, w1, w2)
+        torch.cuda.synchronize()
+        outs.append((y.clone(), *[t.clone() for t in g]))
+        layer.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
