@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -37,13 +38,22 @@ struct moe_ctx {
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
-  enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, NWIN = 6 };
+  enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, W_FLAGS = 6, NWIN = 7 };
+  uint32_t epoch = 0;  // flag-barrier epoch
   void* win[NWIN] = {};
   std::vector<void*> opened;
   void** d_table = nullptr;  // device [world][NWIN]
   Piece* d_disp = nullptr;
   Piece* d_ret = nullptr;
   int n_disp = 0, n_ret = 0;
+  std::vector<Piece> h_ret;        // return pieces (host copy, for copy-engine exchanges)
+  Piece* d_ret_local = nullptr;    // this rank's own return pieces (SM copy kernel)
+  int n_ret_local = 0;
+  std::vector<int> h_ret_el;       // local expert of each return piece
+  std::vector<void*> h_table;      // [world][NWIN] peer-mapped pointers
+  cudaStream_t side = nullptr;     // copy-engine / overlap stream
+  bool overlap = true;             // MOE_NO_OVERLAP=1: serial return exchanges (A/B knob)
+  cudaEvent_t ev[4] = {};
   int64_t disp_bytes[3] = {0, 0, 0}, ret_bytes[3] = {0, 0, 0};  // by Piece::kind
   float* d_barrier = nullptr;
   uint64_t gen = 0;
@@ -201,27 +211,33 @@ moe_status ag_expert(moe_ctx* c, int pass, void* X, cudaStream_t st) {
 }
 
 // F8/B7 under DTD: in-place reduce-scatter of expert space over TP (AR + drop = RS).
-moe_status rs_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st) {
+moe_status rs_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st, int el_lo = 0, int el_hi = -1,
+                     bool count = true) {
   const Dims& d = c->d;
   const size_t cnt = (size_t)d.Gep * d.Cs * d.H;
+  if (el_hi < 0) el_hi = d.El;
   NCCL_TRY(c, ncclGroupStart());
-  for (int el = 0; el < d.El; ++el) {
+  for (int el = el_lo; el < el_hi; ++el) {
     uint8_t* base = at<uint8_t>(Y, (size_t)el * d.R * d.H * 2);
     NCCL_TRY(c, ncclReduceScatter(base, base + (size_t)d.t * cnt * 2, cnt, ncclBfloat16, ncclSum,
                                   c->tp_comm, st));
   }
   NCCL_TRY(c, ncclGroupEnd());
   const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
-  ledger(c, MOE_COLL_REDUCESCATTER, pass, xe * (d.Gt - 1) / d.Gt);
+  if (count) ledger(c, MOE_COLL_REDUCESCATTER, pass, xe * (d.Gt - 1) / d.Gt);
   return MOE_OK;
 }
 
 // F8/B7 vanilla: the Megatron all-reduce of the row-parallel partials.
-moe_status ar_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st) {
+moe_status ar_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st, int el_lo = 0, int el_hi = -1,
+                     bool count = true) {
   const Dims& d = c->d;
-  const size_t cnt = (size_t)d.El * d.R * d.H;
-  NCCL_TRY(c, ncclAllReduce(Y, Y, cnt, ncclBfloat16, ncclSum, c->tp_comm, st));
-  ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * (int64_t)cnt * 2 * (d.Gt - 1) / d.Gt);
+  if (el_hi < 0) el_hi = d.El;
+  const size_t per = (size_t)d.R * d.H;
+  uint8_t* base = at<uint8_t>(Y, (size_t)el_lo * per * 2);
+  NCCL_TRY(c, ncclAllReduce(base, base, per * (el_hi - el_lo), ncclBfloat16, ncclSum, c->tp_comm, st));
+  const size_t cnt = (size_t)d.El * per;
+  if (count) ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * (int64_t)cnt * 2 * (d.Gt - 1) / d.Gt);
   return MOE_OK;
 }
 
@@ -260,7 +276,8 @@ moe_status gemm(moe_ctx* c, const GemmArgs& g, cudaStream_t st) {
 // after the TP reduction) into slot-space windows (WO, WdS). Under DTD a rank
 // sends only its slot slice t, to every TP rank of the destination (the folded
 // all-gather); vanilla sends all slices to the same-t rank only.
-void build_pieces(const Dims& d, bool dispatch, std::vector<Piece>& v, int64_t bytes[3]) {
+void build_pieces(const Dims& d, bool dispatch, std::vector<Piece>& v, int64_t bytes[3],
+                  std::vector<int>* els = nullptr) {
   const uint64_t pb = (uint64_t)d.Cs * d.H * 2;
   const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
   auto rank_of = [&](int ep, int t) { return (d.d * d.Gep + ep) * d.Gt + t; };
@@ -297,6 +314,7 @@ void build_pieces(const Dims& d, bool dispatch, std::vector<Piece>& v, int64_t b
             for (int t2 = 0; t2 < d.Gt; ++t2) push(so, dof, src, t2);
           else
             push(so, dof, src, d.t);
+          if (els) els->resize(v.size(), el);
         }
     }
   }
@@ -307,7 +325,7 @@ moe_status setup_peer(moe_ctx* c) {
   const size_t expert_space = (size_t)d.El * d.R * d.H * 2;
   const size_t slot_space = (size_t)d.E * d.C * d.H * 2;
   const size_t sizes[moe_ctx::NWIN] = {expert_space, expert_space, slot_space, slot_space,
-                                       expert_space, slot_space};
+                                       expert_space, slot_space, (size_t)256 * ((d.world + 63) / 64)};
   std::vector<cudaIpcMemHandle_t> mine(moe_ctx::NWIN);
   for (int w = 0; w < moe_ctx::NWIN; ++w) {
     CUDA_TRY(c, cudaMalloc(&c->win[w], sizes[w]));
@@ -342,7 +360,17 @@ moe_status setup_peer(moe_ctx* c) {
   CUDA_TRY(c, cudaMemcpy(c->d_table, table.data(), sizeof(void*) * table.size(), cudaMemcpyHostToDevice));
   std::vector<Piece> disp, ret;
   build_pieces(d, true, disp, c->disp_bytes);
-  build_pieces(d, false, ret, c->ret_bytes);
+  build_pieces(d, false, ret, c->ret_bytes, &c->h_ret_el);
+  c->h_ret = ret;
+  c->h_table = table;
+  std::vector<Piece> loc;
+  for (const Piece& p : ret)
+    if (p.dst_rank == d.rank) loc.push_back(p);
+  c->n_ret_local = (int)loc.size();
+  CUDA_TRY(c, cudaMalloc(&c->d_ret_local, sizeof(Piece) * (loc.size() + 1)));
+  CUDA_TRY(c, cudaMemcpy(c->d_ret_local, loc.data(), sizeof(Piece) * loc.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   c->n_disp = (int)disp.size();
   c->n_ret = (int)ret.size();
   CUDA_TRY(c, cudaMalloc(&c->d_disp, sizeof(Piece) * (disp.size() + 1)));
@@ -356,6 +384,9 @@ moe_status setup_peer(moe_ctx* c) {
 }
 
 void teardown_peer(moe_ctx* c) {
+  if (c->side) cudaStreamDestroy(c->side);
+  for (int i = 0; i < 4; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   c->opened.clear();
   for (int w = 0; w < moe_ctx::NWIN; ++w)
@@ -363,6 +394,7 @@ void teardown_peer(moe_ctx* c) {
   if (c->d_table) cudaFree(c->d_table);
   if (c->d_disp) cudaFree(c->d_disp);
   if (c->d_ret) cudaFree(c->d_ret);
+  if (c->d_ret_local) cudaFree(c->d_ret_local);
   if (c->d_barrier) cudaFree(c->d_barrier);
 }
 
@@ -377,10 +409,50 @@ PeerDst peer_dst(const moe_ctx* c, int win) {
   return pd;
 }
 
+#define TRY0(expr)                        \
+  do {                                    \
+    moe_status _s0 = (expr);              \
+    if (_s0 != MOE_OK) return _s0;        \
+  } while (0)
+
+// Return-direction exchange of the remote pieces on the copy engines (no SMs): one peer
+// cudaMemcpyAsync per piece of local experts [el_lo, el_hi), so it overlaps a persistent
+// GEMM. This rank's own pieces go through exchange_local (an SM copy kernel), since a
+// same-device memcpy would itself wait for free SMs.
+moe_status exchange_ce(moe_ctx* c, const void* src, int win, int el_lo, int el_hi, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t pb = (size_t)d.Cs * d.H * 2;
+  for (size_t i = 0; i < c->h_ret.size(); ++i) {
+    const int el = c->h_ret_el[i];
+    if (el < el_lo || el >= el_hi) continue;
+    const Piece& p = c->h_ret[i];
+    if (p.dst_rank == d.rank) continue;
+    uint8_t* dst = static_cast<uint8_t*>(c->h_table[(size_t)p.dst_rank * moe_ctx::NWIN + win]) + p.dst_off;
+    CUDA_TRY(c, cudaMemcpyAsync(dst, static_cast<const uint8_t*>(src) + p.src_off, pb,
+                                cudaMemcpyDeviceToDevice, st));
+  }
+  return MOE_OK;
+}
+
+moe_status exchange_local(moe_ctx* c, const void* src, int win, cudaStream_t st) {
+  const Dims& d = c->d;
+  CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, c->d_ret_local, c->n_ret_local,
+                            (size_t)d.Cs * d.H * 2, st));
+  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  return MOE_OK;
+}
+
+moe_status barrier(moe_ctx* c, cudaStream_t st) {
+  const Dims& d = c->d;
+  CUDA_TRY(c, peer_barrier(c->d_table, moe_ctx::NWIN, moe_ctx::W_FLAGS, d.world, d.rank, ++c->epoch, st));
+  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  return MOE_OK;
+}
+
 // Barrier publishing a fused peer write (dispatch / combine-backward) + ledger.
 moe_status publish(moe_ctx* c, bool dispatch, int pass, cudaStream_t st) {
   const Dims& d = c->d;
-  NCCL_TRY(c, ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclFloat32, ncclSum, c->world_comm, st));
+  TRY0(barrier(c, st));
   const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
   if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);
@@ -395,7 +467,7 @@ moe_status exchange(moe_ctx* c, bool dispatch, int pass, const void* src, int wi
   CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, dispatch ? c->d_disp : c->d_ret,
                             dispatch ? c->n_disp : c->n_ret, pb, st));
   c->stats.kernel_launches[MOE_K_COMM] += 1;
-  NCCL_TRY(c, ncclAllReduce(c->d_barrier, c->d_barrier, 1, ncclFloat32, ncclSum, c->world_comm, st));
+  TRY0(barrier(c, st));
   const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
   if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);
@@ -458,25 +530,50 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
   GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
   TRY(gemm(c, g1, st));
-  GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
-  TRY(gemm(c, g2, st));
-
-  // F8 TP reduce, F9 a2a back, F10 all-gather
-  if (!solo) {
+  if (d.peer) {
+    // F7 GEMM2 in two expert halves; each half's TP reduction and return pieces (F8-F10)
+    // go out on the side stream (copy engines) while the next half computes
+    const int h = c->overlap && d.El >= 2 && d.Gt == 1 ? d.El / 2 : d.El;
+    const size_t rows = (size_t)d.R * d.H;
+    for (int part = 0; part < 2; ++part) {
+      const int e0 = part == 0 ? 0 : h, e1 = part == 0 ? h : d.El;
+      if (e1 <= e0) continue;
+      const size_t ao = (size_t)e0 * d.R * d.Fl * 2, yo = (size_t)e0 * rows * 2;
+      GemmArgs g2{e1 - e0, (int)d.R, d.H, d.Fl, at<uint8_t>(A, ao), 0,
+                  at<uint8_t>(const_cast<void*>(w2), (size_t)e0 * d.H * d.Fl * 2), 0,
+                  at<uint8_t>(Y, yo), EPI_STORE, nullptr};
+      TRY(gemm(c, g2, st));
+      CUDA_TRY(c, cudaEventRecord(c->ev[part], st));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[part], 0));
+      if (d.Gt > 1) {
+        if (d.dtd) TRY(rs_expert(c, pass, Y, c->side, e0, e1, e0 == 0));
+        else TRY(ar_expert(c, pass, Y, c->side, e0, e1, e0 == 0));
+      }
+      TRY(exchange_ce(c, Y, moe_ctx::W_O0 + rslot, e0, e1, c->side));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[2], c->side));
     Scope sc_(c, MOE_K_COMM, st, 0);
-    if (d.Gt > 1) {
-      if (d.dtd) TRY(rs_expert(c, pass, Y, st));
-      else TRY(ar_expert(c, pass, Y, st));
-    }
-    if (d.peer) {
-      TRY(exchange(c, false, pass, Y, moe_ctx::W_O0 + rslot, st));
-    } else {
-      TRY(ep_exchange(c, 1, pass, O, Y, lo, hi, st));
-      if (d.dtd) TRY(ag_slot(c, pass, O, st));
-    }
-    if (d.peer && d.ckpt) {  // CAC stash of the second collective's output
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[2], 0));
+    TRY(exchange_local(c, Y, moe_ctx::W_O0 + rslot, st));
+    TRY(barrier(c, st));
+    if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
+    if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
+    if (d.ckpt) {  // CAC stash of the second collective's output
       CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.O), O, (size_t)d.E * d.C * d.H * 2,
                                   cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+    TRY(gemm(c, g2, st));
+    // F8 TP reduce, F9 a2a back, F10 all-gather
+    if (!solo) {
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      if (d.Gt > 1) {
+        if (d.dtd) TRY(rs_expert(c, pass, Y, st));
+        else TRY(ar_expert(c, pass, Y, st));
+      }
+      TRY(ep_exchange(c, 1, pass, O, Y, lo, hi, st));
+      if (d.dtd) TRY(ag_slot(c, pass, O, st));
     }
   }
 
@@ -595,6 +692,8 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
       return fail(MOE_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
     }
     if (d.peer) {
+      const char* no = std::getenv("MOE_NO_OVERLAP");
+      c->overlap = !(no && no[0] == '1');
       moe_status ps = setup_peer(c);
       if (ps != MOE_OK) {
         const std::string why2 = g_detail;
@@ -743,19 +842,44 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
   TRY(gemm(c, g5, st));
   GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};
-  TRY(gemm(c, g6, st));
   GemmArgs g7{d.El, d.Fl, d.H, (int)d.R, dH, 1, X, 1, dw1, EPI_STORE, nullptr};
-  TRY(gemm(c, g7, st));
-  // B7 TP reduce, B8 a2a back, B9 all-gather
-  if (!solo) {
-    Scope sc_(c, MOE_K_COMM, st, 0);
-    if (d.Gt > 1) {
-      if (d.dtd) TRY(rs_expert(c, 1, dXp, st));
-      else TRY(ar_expert(c, 1, dXp, st));
+  if (d.peer) {
+    // B7-B9 (TP reduction + return pieces) on the side stream, overlapping the
+    // weight-gradient GEMMs, which do not feed them
+    CUDA_TRY(c, cudaEventRecord(c->ev[0], st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[0], 0));
+    if (!c->overlap) {
+      TRY(gemm(c, g6, st));
+      TRY(gemm(c, g7, st));
+      CUDA_TRY(c, cudaEventRecord(c->ev[0], st));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[0], 0));
     }
-    if (d.peer) {
-      TRY(exchange(c, false, 1, dXp, moe_ctx::W_DS, st));
-    } else {
+    if (d.Gt > 1) {
+      if (d.dtd) TRY(rs_expert(c, 1, dXp, c->side));
+      else TRY(ar_expert(c, 1, dXp, c->side));
+    }
+    TRY(exchange_ce(c, dXp, moe_ctx::W_DS, 0, d.El, c->side));
+    CUDA_TRY(c, cudaEventRecord(c->ev[1], c->side));
+    if (c->overlap) {
+      TRY(gemm(c, g6, st));
+      TRY(gemm(c, g7, st));
+    }
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[1], 0));
+    TRY(exchange_local(c, dXp, moe_ctx::W_DS, st));
+    TRY(barrier(c, st));
+    if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
+    if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
+  } else {
+    TRY(gemm(c, g6, st));
+    TRY(gemm(c, g7, st));
+    // B7 TP reduce, B8 a2a back, B9 all-gather
+    if (!solo) {
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      if (d.Gt > 1) {
+        if (d.dtd) TRY(rs_expert(c, 1, dXp, st));
+        else TRY(ar_expert(c, 1, dXp, st));
+      }
       TRY(ep_exchange(c, 1, 1, dS, dXp, lo, hi, st));
       if (d.dtd) TRY(ag_slot(c, 1, dS, st));
     }

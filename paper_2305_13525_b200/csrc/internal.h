@@ -90,6 +90,9 @@ struct Piece {
 };
 cudaError_t peer_exchange(const void* src, void* const* d_table, int nwin, int win,
                           const Piece* d_pieces, int npieces, size_t piece_bytes, cudaStream_t s);
+// Flag barrier over the peer windows (window `win` holds one uint32 slot per rank).
+cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
+                         uint32_t epoch, cudaStream_t s);
 
 // Destination of slot-space rows in the expert-space windows of the EP/TP peers
 // (fused dispatch / combine-backward): slot (tt, e, cs) of this rank lands at

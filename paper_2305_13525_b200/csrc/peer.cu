@@ -40,7 +40,31 @@ __global__ void __launch_bounds__(XC_THREADS)
   __threadfence_system();
 }
 
+// Cross-rank barrier over peer memory: thread r stores `epoch` into rank r's flag
+// slot for this rank (release, system scope), then acquire-spins until rank r has
+// stored `epoch` into ours. Launched after the copy kernel it publishes (stream
+// order), so every write of that kernel precedes the flag.
+__global__ void peer_barrier_kernel(void* const* __restrict__ table, int nwin, int win, int world,
+                                    int rank, uint32_t epoch) {
+  const int r = threadIdx.x;
+  if (r >= world) return;
+  uint32_t* remote = static_cast<uint32_t*>(table[(size_t)r * nwin + win]);
+  uint32_t* mine = static_cast<uint32_t*>(table[(size_t)rank * nwin + win]);
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote + rank), "r"(epoch) : "memory");
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + r) : "memory");
+  } while ((int32_t)(v - epoch) < 0);
+}
+
 }  // namespace
+
+cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
+                         uint32_t epoch, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 32 * ((world + 31) / 32), 0, s>>>(d_table, nwin, win, world, rank, epoch);
+  return cudaGetLastError();
+}
 
 cudaError_t peer_exchange(const void* src, void* const* d_table, int nwin, int win,
                           const Piece* d_pieces, int npieces, size_t piece_bytes, cudaStream_t s) {
