@@ -13,7 +13,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmoe.so")
+# MOE_LIB_PATH: development A/B of two builds of this library (tools/ab_lib.sh)
+LIB_PATH = os.environ.get("MOE_LIB_PATH") or os.path.join(_PKG, "libmoe.so")
 
 MOE_F_STATS = 1
 MOE_F_FORCED_ROUTING = 2

@@ -391,4 +391,13 @@ __device__ __forceinline__ float2 gelu_grad2(float2 h) {
   return f2fma(f2mul(f2mul(kh, make_float2(0.5f, 0.5f)), s), b, a);
 }
 
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(addr)
+               : "memory");
+  return r;
+}
+
 }  // namespace moe

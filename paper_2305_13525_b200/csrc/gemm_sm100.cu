@@ -274,17 +274,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // both arrive on the leader's tmem-empty barrier.
 constexpr int A2_STAGE = 128 * BK * 2;  // 16 KiB
 constexpr int B2_STAGE = 128 * BK * 2;  // 16 KiB (this CTA's half of BN = 256)
-constexpr int EPI_WARPS = 8;            // 2 per TMEM lane quadrant, each half of the 256 columns
-constexpr int NUM_THREADS2 = (4 + EPI_WARPS) * 32;
+constexpr int STAGES2 = 6;
 constexpr int EPI_BUF = 32 * 32 * 2;  // one warp's 32 x 32 bf16 chunk, 64B-swizzled
-// per epilogue warp: 2 staging buffers per output (D, and A = gelu for EPI_GELU);
-// the two-output GeLU variant gives up one pipeline stage to fit
+// Epilogue warps: 4 per 64 columns (one per TMEM lane quadrant). The plain and
+// dGeLU epilogues use 16 (each warp drains 32 rows x 64 columns per tile); the
+// GeLU epilogue (two outputs, ~110 registers) uses 8 (32 rows x 128 columns).
 __host__ __device__ constexpr int epi_outs(int epi) { return epi == EPI_GELU ? 2 : 1; }
-__host__ __device__ constexpr int stages2(int epi) { return epi == EPI_GELU ? 5 : 6; }
-__host__ __device__ constexpr int epi_smem(int epi) { return EPI_WARPS * 2 * epi_outs(epi) * EPI_BUF; }
+__host__ __device__ constexpr int epi_warps(int epi) { return epi == EPI_GELU ? 8 : 16; }
+__host__ __device__ constexpr int threads2(int epi) { return (4 + epi_warps(epi)) * 32; }
+__host__ __device__ constexpr int epi_smem(int epi) { return epi_warps(epi) * epi_outs(epi) * EPI_BUF; }
 __host__ __device__ constexpr int smem2_bytes(int epi) {
-  return stages2(epi) * (A2_STAGE + B2_STAGE) + epi_smem(epi) + 1024 + 256;
+  return STAGES2 * (A2_STAGE + B2_STAGE) + epi_smem(epi) + 1024 + 256;
 }
+static_assert(smem2_bytes(EPI_STORE) <= 227 * 1024 && smem2_bytes(EPI_GELU) <= 227 * 1024, "smem");
 
 __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
@@ -292,19 +294,19 @@ __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
 }
 
 template <int A_MN, int B_MN, int EPI>
-__global__ void __launch_bounds__(NUM_THREADS2, 1)
+__global__ void __launch_bounds__(threads2(EPI), 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX,
                  const Params p) {
-  constexpr int STAGES2 = stages2(EPI);
-  constexpr int EPI_SMEM = epi_smem(EPI);
+  constexpr int EW = epi_warps(EPI);
+  constexpr int NO = epi_outs(EPI);
+  constexpr int COLS_W = BN / (EW / 4);  // columns one epilogue warp drains per tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES2 * A2_STAGE;
-  uint8_t* smE = smB + STAGES2 * B2_STAGE;  // epilogue staging (1024-aligned)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smE + EPI_SMEM);
+  uint8_t* smE = smB + STAGES2 * B2_STAGE;  // epilogue transpose buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smE + epi_smem(EPI));
   // [0,S) full (leader's counts both CTAs), [S,2S) empty, [2S,2S+2) tmem_full, [2S+2,2S+4) tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES2 + 4);
 
@@ -318,15 +320,13 @@ __global__ void __launch_bounds__(NUM_THREADS2, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    tma_prefetch_desc(&tmD);
-    if (EPI == EPI_GELU) tma_prefetch_desc(&tmX);
     for (int s = 0; s < STAGES2; ++s) {
       mbar_init(smem_u32(&bars[s]), 1);
       mbar_init(smem_u32(&bars[STAGES2 + s]), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&bars[2 * STAGES2 + a]), 1);
-      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
+      mbar_init(smem_u32(&bars[2 * STAGES2 + 2 + a]), 2 * EW);  // epilogue warps x 2 CTAs
     }
     fence_barrier_init();
   }
@@ -412,17 +412,18 @@ __global__ void __launch_bounds__(NUM_THREADS2, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    // TMEM -> registers -> (epilogue math) -> bf16 -> 64B-swizzled smem chunk of
-    // 32 rows x 32 cols -> TMA bulk-tensor store (coalesced; rows >= M and
-    // columns >= N are clipped by the tensor map). Two buffers per output per
-    // warp; a buffer is rewritten only after its previous store has been read.
+    // TMEM -> registers (lane = row, 32 fp32 columns) -> epilogue math -> bf16 ->
+    // this warp's 64B-swizzled 32 x 32 smem buffer -> read back 8 rows x 64 B per
+    // instruction -> st.global.v4 (full 32 B sectors). Rows >= M and columns >= N
+    // are skipped. No async proxy on the store side: a chunk costs two __syncwarp.
     const int ew = warp - 4;
-    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
-    const int col0 = (ew >> 2) * (BN / 2);  // this warp's half of the columns
-    constexpr int NO = epi_outs(EPI);
-    const uint32_t ebase = smem_u32(smE) + ew * 2 * NO * EPI_BUF;
+    const int quad = warp & 3;              // TMEM lane quadrant this warp may access
+    const int col0 = (ew >> 2) * COLS_W;    // this warp's column slice of the tile
+    const uint32_t bD = smem_u32(smE) + ew * NO * EPI_BUF;
+    const uint32_t bX = bD + EPI_BUF;
     const uint32_t swz = (uint32_t)((lane >> 1) & 3);
-    int iter = 0, chunk_ctr = 0;
+    const int rr = lane >> 2, qq = lane & 3;  // read-back: row within an 8-row group, 16 B piece
+    int iter = 0;
     for (int tile = cluster; tile < p.total_tiles; tile += nclusters, ++iter) {
       const int b = tile / tiles_mn;
       const int r = tile - b * tiles_mn;
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(NUM_THREADS2, 1)
       const bool row_ok = m < p.M;
       const size_t row_off = ((size_t)b * p.M + (row_ok ? m : 0)) * (size_t)p.N;
 #pragma unroll 1
-      for (int c = col0; c < col0 + BN / 2; c += 32) {
+      for (int c = col0; c < col0 + COLS_W; c += 32) {
         const int n = n0 + c;
         if (n >= p.N) break;  // uniform across the warp
         uint32_t v[32];
@@ -470,32 +471,34 @@ __global__ void __launch_bounds__(NUM_THREADS2, 1)
             o[w] = pack_bf16x2(f.x, f.y);
           }
         }
-        const int bi = chunk_ctr & 1;
-        ++chunk_ctr;
-        if (lane == 0) bulk_wait_read_1();
-        __syncwarp();
-        const uint32_t bufD = ebase + bi * EPI_BUF;
-        const uint32_t bufX = ebase + (2 + bi) * EPI_BUF;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t off = lane * 64 + ((q ^ swz) << 4);
-          st_shared_v4(bufD + off, o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-          if (EPI == EPI_GELU) st_shared_v4(bufX + off, g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+          st_shared_v4(bD + off, o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          if (EPI == EPI_GELU) st_shared_v4(bX + off, g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
         }
-        fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          tma_store_3d(&tmD, bufD, n, mrow0, b);
-          if (EPI == EPI_GELU) tma_store_3d(&tmX, bufX, n, mrow0, b);
-          bulk_commit();
+        const bool col_ok = n + qq * 8 < p.N;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = i * 8 + rr;
+          const uint32_t off = row * 64 + ((qq ^ ((row >> 1) & 3)) << 4);
+          const int mm = mrow0 + row;
+          const bool ok = mm < p.M && col_ok;
+          const size_t go = ((size_t)b * p.M + mm) * (size_t)p.N + n + qq * 8;
+          const uint4 vd = ld_shared_v4(bD + off);
+          if (ok) st_v4(p.D + go, vd);
+          if (EPI == EPI_GELU) {
+            const uint4 vx = ld_shared_v4(bX + off);
+            if (ok) st_v4(p.aux + go, vx);
+          }
         }
+        __syncwarp();  // the buffer is rewritten by the next chunk
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(smem_u32(&bars[2 * STAGES2 + 2 + acc]), 0);
     }
-    if (lane == 0) bulk_wait_all();
-    __syncwarp();
   }
 
   tc_fence_before();
@@ -555,8 +558,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
 }
 
 template <int A_MN, int B_MN, int EPI>
-cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
-                    const CUtensorMap& tx, const Params& p, cudaStream_t s) {
+cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
   static bool attr = false;
   auto k = gemm2_kernel<A_MN, B_MN, EPI>;
   constexpr int SMEM2_BYTES = smem2_bytes(EPI);
@@ -569,7 +571,7 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensor
   if (p.total_tiles < clusters) clusters = p.total_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * clusters);
-  cfg.blockDim = dim3(NUM_THREADS2);
+  cfg.blockDim = dim3(threads2(EPI));
   cfg.dynamicSmemBytes = SMEM2_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
@@ -579,7 +581,7 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensor
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, ta, tb, td, tx, p);
+  return cudaLaunchKernelEx(&cfg, k, ta, tb, p);
 }
 
 }  // namespace
@@ -605,18 +607,12 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   p.aux = static_cast<bf16*>(a.aux);
   const int key = a.a_mn * 100 + a.b_mn * 10 + a.epilogue;
   if (pair) {
-    CUtensorMap td, tx;
-    bool okd = make_map(&td, a.D, a.N, a.M, a.batch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-    okd = okd && (a.epilogue != EPI_GELU ||
-                  make_map(&tx, a.aux, a.N, a.M, a.batch, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
-    if (a.epilogue != EPI_GELU) tx = td;
-    if (!okd) { *why = "cuTensorMapEncodeTiled rejected the output layout"; return cudaErrorInvalidValue; }
     switch (key) {
-      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, td, tx, p, s);
-      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, td, tx, p, s);
-      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, td, tx, p, s);
-      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, td, tx, p, s);
-      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, td, tx, p, s);
+      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, p, s);
+      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, p, s);
+      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, p, s);
+      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, p, s);
+      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, p, s);
       default: break;
     }
   } else {
