@@ -45,7 +45,44 @@ def parse():
     p.add_argument("--vanilla", action="store_true", help="disable DTD (G_tensor > 1 configs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-optim", action="store_true", help="skip the tiled-optimizer measurement")
     return p.parse_args()
+
+
+def measure_optimizer(dw1, dw2, peaks, steps, dev):
+    """NEXT #3 (include/moe_optim.h): AdamW over this rank's expert parameters, whose bf16
+    gradients the layer just produced (dW1, dW2). Fused (no temporary) vs the paper's
+    tiled step (ts = 1.8 M, 4*ts-byte buffer, 2 launches per tile). Not part of `value`."""
+    from paper_2305_13525_b200 import MOE_TILE_PARAMS_PAPER, moe_adamw_plan, moe_adamw_step
+    n = dw1.numel() + dw2.numel()
+    g = torch.cat([dw1.reshape(-1), dw2.reshape(-1)])
+    gen = torch.Generator(device=dev).manual_seed(BASE_SEED + 7000)
+    p = torch.randn(n, generator=gen, device=dev) * 0.02
+    m = torch.zeros(n, device=dev)
+    v = torch.zeros(n, device=dev)
+    p16 = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    ts = MOE_TILE_PARAMS_PAPER
+    n_tiles, temp_bytes = moe_adamw_plan(n, ts)
+    temp = torch.empty(temp_bytes // 4, device=dev)
+    hp = dict(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+    out = {"params": n, "tile_params": ts, "tiles": n_tiles, "temp_bytes_tiled": temp_bytes,
+           "temp_bytes_untiled_upcast": 4 * n, "temp_bytes_fused": 0}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(3, min(steps, 10))
+    for name, tp, tmp, bpp, launches in (("fused", 0, None, 28, 1), ("tiled", ts, temp, 36, 2 * n_tiles)):
+        for i in range(2):
+            moe_adamw_step(g, p, m, v, p16, step=1 + i, tile_params=tp, temp=tmp, **hp)
+        torch.cuda.synchronize()
+        e0.record()
+        for i in range(k):
+            moe_adamw_step(g, p, m, v, p16, step=3 + i, tile_params=tp, temp=tmp, **hp)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        gbs = bpp * n / (ms / 1e3) / 1e9
+        out[name] = {"ms": ms, "params_per_s": n / (ms / 1e3), "bytes_per_param": bpp, "GB/s": gbs,
+                     "frac": gbs / peaks["hbm_gbs"], "launches": launches}
+    return out
 
 
 def workload(args, world):
@@ -396,6 +433,10 @@ def main():
                "what": "pinned host x, dy -> device; moe_forward + moe_backward; y, dx -> host; "
                        "H2D / D2H on their own streams, double-buffered (next step's H2D overlaps this step's compute)"}
 
+    optim = None
+    if not args.no_optim:
+        optim = measure_optimizer(grads[2], grads[3], peaks, args.steps, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(H, F, E)
@@ -414,7 +455,8 @@ def main():
                "launches_per_step": launches_per_step, "clocks": clk,
                "kernel_ms_per_step": per_class,
                "dropped_tokens": st["dropped_tokens"], "tie_tokens": st["tie_tokens"],
-               "collectives": {"calls": st["calls"], "wire_bytes": st["wire_bytes"]}}
+               "collectives": {"calls": st["calls"], "wire_bytes": st["wire_bytes"]},
+               "optimizer": optim}
         if world > 1:
             a2a_ms = per_class["comm"]
             out["comm_ms_per_step"] = a2a_ms

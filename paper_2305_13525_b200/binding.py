@@ -64,10 +64,15 @@ class _Stats(ctypes.Structure):
                 ("replay_calls", ctypes.c_int64)]
 
 
+class _AdamW(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("step", ctypes.c_int64)]
+
+
 EXPORTS = ("moe_plan_layout", "moe_plan_bytes", "moe_plan_collectives", "moe_get_unique_id",
            "moe_create", "moe_forward", "moe_backward", "moe_forward_replay", "moe_routing", "moe_stats_get",
            "moe_stats_reset", "moe_destroy", "moe_status_string", "moe_last_error_detail",
-           "moe_gemm_bf16")
+           "moe_gemm_bf16", "moe_adamw_plan", "moe_adamw_step")
 
 _lib = None
 
@@ -99,6 +104,9 @@ def lib() -> ctypes.CDLL:
     L.moe_status_string.restype = ctypes.c_char_p
     L.moe_last_error_detail.restype = ctypes.c_char_p
     L.moe_gemm_bf16.argtypes = [I, I, I, I, P, I, P, I, P, I, P, I, P]
+    I64 = ctypes.c_int64
+    L.moe_adamw_plan.argtypes = [I64, I64, ctypes.POINTER(I64), ctypes.POINTER(SZ)]
+    L.moe_adamw_step.argtypes = [P, P, P, P, P, I64, ctypes.POINTER(_AdamW), I64, P, P]
     for name in EXPORTS:
         if name not in ("moe_status_string", "moe_last_error_detail"):
             getattr(L, name).restype = ctypes.c_int
@@ -181,6 +189,27 @@ def moe_gemm_bf16(A, B, D, a_mn: int, b_mn: int, epilogue: int = 0, aux=None, im
     K = A.shape[2] if not a_mn else A.shape[1]
     _check(lib().moe_gemm_bf16(batch, M, N, K, _ptr(A), a_mn, _ptr(B), b_mn, _ptr(D), epilogue,
                                _ptr(aux), impl, _stream(stream)))
+
+
+MOE_TILE_PARAMS_PAPER = 1_800_000  # include/moe_optim.h
+
+
+def moe_adamw_plan(n: int, tile_params: int):
+    """(n_tiles, temp_bytes) of the tiled optimizer step (include/moe_optim.h)."""
+    nt, tb = ctypes.c_int64(), ctypes.c_size_t()
+    _check(lib().moe_adamw_plan(n, tile_params, ctypes.byref(nt), ctypes.byref(tb)))
+    return nt.value, tb.value
+
+
+def moe_adamw_step(grad, master, exp_avg, exp_avg_sq, param=None, *, lr: float, beta1: float,
+                   beta2: float, eps: float, weight_decay: float, step: int, tile_params: int = 0,
+                   temp=None, stream=None):
+    """One AdamW step of include/moe_optim.h: grad/param bf16, the rest fp32, same numel;
+    tile_params > 0 runs the paper's tiled step with `temp` (fp32, >= plan temp bytes)."""
+    n = master.numel()
+    h = _AdamW(lr, beta1, beta2, eps, weight_decay, step)
+    _check(lib().moe_adamw_step(_ptr(grad), _ptr(master), _ptr(exp_avg), _ptr(exp_avg_sq), _ptr(param), n,
+                                ctypes.byref(h), tile_params, _ptr(temp), _stream(stream)))
 
 
 class MoELayer:

@@ -16,7 +16,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmoe.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["gemm_sm100.cu", "route.cu", "permute.cu", "gate_bwd.cu", "peer.cu", "plan.cpp", "api.cpp"]
+SOURCES = ["gemm_sm100.cu", "route.cu", "permute.cu", "gate_bwd.cu", "peer.cu", "optim.cu", "plan.cpp", "api.cpp"]
 
 
 def nccl_dirs() -> tuple[str, str]:
@@ -30,7 +30,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(ROOT, "include", "moe.h"))
+    deps += [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
 

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "../../include/moe.h"
+#include "../../include/moe_optim.h"
 #include "internal.h"
 #include "plan.h"
 
@@ -1003,6 +1005,54 @@ moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn
     return MOE_OK;
   }
   return gemm(nullptr, g, st);
+}
+
+moe_status moe_adamw_plan(int64_t n, int64_t tile_params, int64_t* n_tiles, size_t* temp_bytes) {
+  if (n < 0 || tile_params < 0 || !n_tiles || !temp_bytes) return fail(MOE_ERR_ARG, "bad arguments");
+  if (tile_params == 0) {
+    *n_tiles = n > 0 ? 1 : 0;
+    *temp_bytes = 0;
+  } else {
+    *n_tiles = (n + tile_params - 1) / tile_params;
+    *temp_bytes = 4 * (size_t)(n < tile_params ? n : tile_params);
+  }
+  return MOE_OK;
+}
+
+moe_status moe_adamw_step(const void* grad, float* master, float* exp_avg, float* exp_avg_sq,
+                          void* param, int64_t n, const moe_adamw_hparams* h, int64_t tile_params,
+                          float* temp, void* stream) {
+  if (!h || n < 0 || tile_params < 0) return fail(MOE_ERR_ARG, "bad arguments");
+  if (h->step < 1) return fail(MOE_ERR_ARG, "step must be >= 1");
+  if (n == 0) return MOE_OK;
+  if (!grad || !master || !exp_avg || !exp_avg_sq) return fail(MOE_ERR_ARG, "null array");
+  if (tile_params > 0 && !temp) return fail(MOE_ERR_ARG, "tiled step needs temp (moe_adamw_plan)");
+  if (tile_params == 0 && temp) return fail(MOE_ERR_ARG, "fused step takes no temp");
+  if (!aligned16(grad) || !aligned16(master) || !aligned16(exp_avg) || !aligned16(exp_avg_sq) ||
+      (param && !aligned16(param)) || (temp && !aligned16(temp)))
+    return fail(MOE_ERR_ALIGN, "arrays must be 16-byte aligned");
+  // per-step scalars: binary64, rounded once to binary32 (reading R19)
+  const double c1 = 1.0 - std::pow(h->beta1, (double)h->step);
+  const double c2 = 1.0 - std::pow(h->beta2, (double)h->step);
+  AdamwScalars s;
+  s.b1 = (float)h->beta1;
+  s.b2 = (float)h->beta2;
+  s.ob1 = (float)(1.0 - h->beta1);
+  s.ob2 = (float)(1.0 - h->beta2);
+  s.step = (float)(h->lr / c1);
+  s.c2s = (float)std::sqrt(c2);
+  s.decay = (float)(1.0 - h->lr * h->weight_decay);
+  s.eps = (float)h->eps;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (tile_params == 0) {
+    e = adamw_fused(grad, master, exp_avg, exp_avg_sq, param, n, s, st);
+  } else {
+    int launches = 0;
+    e = adamw_tiled(grad, master, exp_avg, exp_avg_sq, param, n, s, tile_params, temp, st, &launches);
+  }
+  if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("adamw: ") + cudaGetErrorString(e));
+  return MOE_OK;
 }
 
 }  // extern "C"

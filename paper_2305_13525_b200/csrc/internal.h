@@ -113,4 +113,14 @@ cudaError_t combine_bwd_peer(const void* dy, const void* O, const int32_t* exper
                              const int32_t* tok_of, const SlotSpace& ss, int64_t T, int t_lo,
                              int t_hi, float* dp, const PeerDst& pd, cudaStream_t s);
 
+// (optim.cu) the tiled optimizer step of include/moe_optim.h: binary32 scalars
+// derived on the host in binary64 (reading R19).
+struct AdamwScalars {
+  float b1, b2, ob1, ob2, step, c2s, decay, eps;
+};
+cudaError_t adamw_fused(const void* grad, float* p, float* m, float* v, void* p16, int64_t n,
+                        const AdamwScalars& s, cudaStream_t st);
+cudaError_t adamw_tiled(const void* grad, float* p, float* m, float* v, void* p16, int64_t n,
+                        const AdamwScalars& s, int64_t ts, float* temp, cudaStream_t st, int* launches);
+
 }  // namespace moe

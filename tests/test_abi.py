@@ -22,7 +22,8 @@ def _built():
 
 
 def header_symbols():
-    src = open(os.path.join(ROOT, "include", "moe.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc)) if f.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(moe_[a-z_0-9]+)\s*\(", src)))
 
