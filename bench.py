@@ -458,8 +458,21 @@ def main():
                "collectives": {"calls": st["calls"], "wire_bytes": st["wire_bytes"]},
                "optimizer": optim}
         if world > 1:
-            a2a_ms = per_class["comm"]
-            out["comm_ms_per_step"] = a2a_ms
+            # a2a bandwidth: bytes this rank sends to other ranks per step over the
+            # time of the kernel classes that move them. In peer mode (default) the dispatch and
+            # combine-backward kernels store straight into the peers' windows and the return
+            # exchanges run in the comm class; their local HBM work is included in the time, so
+            # the figure is a lower bound on the link rate.
+            wb = {k: v / args.steps for k, v in st["wire_bytes"].items()}
+            egress = sum(wb.values())
+            ex_ms = per_class["comm"] + per_class["dispatch"] + per_class["combine_bwd"]
+            gbs = egress / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None
+            out["comm_ms_per_step"] = per_class["comm"]
+            out["a2a"] = {"a2a_bytes_per_step": wb["a2a"], "egress_bytes_per_step": egress,
+                          "exchange_ms_per_step": ex_ms, "egress_GB/s": gbs,
+                          "peak_GB/s": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                          "frac": gbs / 770.0 if gbs else None,
+                          "time_basis": "comm + dispatch + combine_bwd kernel classes (CUDA events)"}
         print(json.dumps(out), flush=True)
     layer.close()
     if dist is not None:

@@ -71,6 +71,18 @@ typedef enum {
                                      issues no collectives (Communication-aware Activation
                                      Checkpointing); without it the replay
                                      re-runs the forward's collectives (plain checkpointing) */
+/* Gating variants (the paper cites the gate's lineage,
+ * PAPER.md:96-97, without defining it): */
+#define MOE_F_RANDOM_PRIORITY 64u /* random token selection (R20): capacity slots
+                                     are granted in a keyed pseudo-random order of the tokens
+                                     (4-round Feistel permutation of [0, T), cycle-walked,
+                                     key = moe_set_priority_seed) instead of token order     */
+#define MOE_F_AUX_LOSS 128u       /* auxiliary load-balancing loss (R21):
+                                     l_aux = aux_loss_coef * E * sum_e f_e P_e per token group,
+                                     f_e = routed fraction, P_e = mean softmax probability;
+                                     moe_forward computes it (moe_aux_loss reads it) and
+                                     moe_backward adds d l_aux / d logits to the gate gradient
+                                     of every token, dropped ones included                   */
 
 /* Layer configuration. Identical on every rank of the job.
  * Constraints (checked, MOE_ERR_SHAPE otherwise):
@@ -88,6 +100,7 @@ typedef struct {
   int32_t g_expert;        /* G_expert                                */
   int32_t dtd;             /* 0 = vanilla (AllReduce + full all-to-all), 1 = DTD       */
   uint32_t flags;          /* MOE_F_*                                                  */
+  float aux_loss_coef;     /* MOE_F_AUX_LOSS coefficient (>= 0; ignored without the flag) */
 } moe_config;
 
 /* Per-rank derived layout (host-only; no GPU needed). */
@@ -213,6 +226,15 @@ moe_status moe_forward_replay(moe_ctx* ctx, const void* saved, const void* x, co
  * count int32 [E] (kept per expert, <= C). Any output may be NULL. */
 moe_status moe_routing(moe_ctx* ctx, const void* saved, int32_t* expert, int32_t* slot,
                        float* prob, float* gap, int32_t* count, void* stream);
+
+/* MOE_F_AUX_LOSS: copies this forward's l_aux (fp32, device pointer, async).
+ * MOE_ERR_STATE without the flag or for a saved blob no forward wrote. */
+moe_status moe_aux_loss(moe_ctx* ctx, const void* saved, float* aux, void* stream);
+
+/* MOE_F_RANDOM_PRIORITY: the key of the priority permutation used by every later
+ * moe_forward on this ctx (default 0). A training loop sets a new key per step;
+ * the same key gives the same slots (the replay and backward use the saved ones). */
+moe_status moe_set_priority_seed(moe_ctx* ctx, uint64_t seed);
 
 /* Ledger + last-forward routing counters + per-class kernel launches/times;
  * synchronizes the ctx's last stream. */

@@ -33,6 +33,7 @@ import numpy as np
 
 __all__ = [
     "decode_bf16", "capacity", "gelu_tanh", "gelu_tanh_grad", "gate", "assign_slots",
+    "priority_order", "aux_loss", "aux_loss_dlogits",
     "Routing", "route", "forward_group", "backward_group", "layer",
     "token_forward", "token_backward", "expert_row_grads", "TIE_GAP",
 ]
@@ -97,22 +98,95 @@ def gate(x: np.ndarray, wg: np.ndarray):
     return logits, expert, gap, s, p
 
 
-def assign_slots(expert: np.ndarray, experts: int, cap: int):
-    """Capacity slots in token order (reading R3).
+def assign_slots(expert: np.ndarray, experts: int, cap: int, order=None):
+    """Capacity slots in priority order (reading R3; NEXT #4 random token selection).
 
-    slot_t = #{t' < t : e*(t') = e*(t)}; kept iff slot_t < C (else slot = -1).
-    Returns (slot [T] int32, count [E] kept per expert, load [E] routed per expert).
+    order: the tokens in priority order (a permutation of range(T)); None is
+    token order, slot_t = #{t' < t : e*(t') = e*(t)}. In general
+    slot_t = #{t' before t in `order` : e*(t') = e*(t)}; kept iff slot_t < C
+    (else slot = -1). Returns (slot [T] int32, count [E] kept per expert,
+    load [E] routed per expert).
     """
     T = expert.shape[0]
     slot = np.full(T, -1, dtype=np.int32)
     seen = np.zeros(experts, dtype=np.int64)
-    for t in range(T):
+    for t in (range(T) if order is None else order):
+        t = int(t)
         e = int(expert[t])
         if seen[e] < cap:
             slot[t] = seen[e]
         seen[e] += 1
     count = np.minimum(seen, cap).astype(np.int32)
     return slot, count, seen.astype(np.int64)
+
+
+# --- NEXT #4 gating variants -------------------------------------------------------
+
+_M32 = 0xFFFFFFFF
+
+
+def _mix32(x: int) -> int:
+    """lowbias32 integer hash (the counter-based generator both sides implement)."""
+    x &= _M32
+    x ^= x >> 16
+    x = (x * 0x7FEB352D) & _M32
+    x ^= x >> 15
+    x = (x * 0x846CA68B) & _M32
+    x ^= x >> 16
+    return x
+
+
+def priority_order(T: int, seed: int) -> np.ndarray:
+    """Random token-selection priority (reading R20): order[i] = sigma(i), a keyed
+    pseudo-random permutation of range(T) — a 4-round Feistel network on the
+    smallest even-width domain 2^(2m) >= T, cycle-walked into [0, T) (a bijection
+    of [0, 2^(2m)) restricted by cycle walking stays a bijection of [0, T)).
+    Round r: (L, R) -> (R, L ^ (mix32(R ^ k_r) & mask)), k_r = (seed_lo*0x9E3779B9 +
+    seed_hi + r*0x85EBCA6B) mod 2^32."""
+    if T <= 0:
+        return np.zeros(0, dtype=np.int64)
+    m = 1
+    while (1 << (2 * m)) < T:
+        m += 1
+    mask = (1 << m) - 1
+    lo, hi = seed & _M32, (seed >> 32) & _M32
+    keys = [((lo * 0x9E3779B9) + hi + r * 0x85EBCA6B) & _M32 for r in range(4)]
+
+    def feistel(x: int) -> int:
+        L, R = x >> m, x & mask
+        for k in keys:
+            L, R = R, L ^ (_mix32(R ^ k) & mask)
+        return (L << m) | R
+
+    out = np.empty(T, dtype=np.int64)
+    for i in range(T):
+        x = feistel(i)
+        while x >= T:
+            x = feistel(x)
+        out[i] = x
+    return out
+
+
+def aux_loss(expert: np.ndarray, s: np.ndarray, coef: float) -> float:
+    """Auxiliary load-balancing loss (reading R21; Switch Transformer eq. 4, GShard):
+    l_aux = coef * E * sum_e f_e P_e, f_e = (1/T) #{t : e*(t) = e} (routed, before
+    capacity), P_e = (1/T) sum_t s_te."""
+    T, E = s.shape
+    if T == 0:
+        return 0.0
+    f = np.bincount(expert, minlength=E) / T
+    P = s.mean(axis=0)
+    return float(coef * E * np.sum(f * P))
+
+
+def aux_loss_dlogits(expert: np.ndarray, s: np.ndarray, coef: float) -> np.ndarray:
+    """d l_aux / d l_tj with f held constant (it is a count):
+    coef * E / T * s_tj (f_j - sum_e f_e s_te), for every token (kept or dropped)."""
+    T, E = s.shape
+    if T == 0:
+        return np.zeros((0, E))
+    f = np.bincount(expert, minlength=E) / T
+    return coef * E / T * s * (f[None, :] - (s @ f)[:, None])
 
 
 @dataclass
@@ -132,7 +206,7 @@ class Routing:
         return self.slot >= 0
 
 
-def route(x: np.ndarray, wg: np.ndarray, cap: int, forced=None, override=None) -> Routing:
+def route(x: np.ndarray, wg: np.ndarray, cap: int, forced=None, override=None, order=None) -> Routing:
     """Gate + slot assignment for one token group.
 
     forced:   int array [T] — expert ids replacing the argmax for every token
@@ -140,6 +214,7 @@ def route(x: np.ndarray, wg: np.ndarray, cap: int, forced=None, override=None) -
     override: (idx, experts) — the tie-override protocol (reading R5): for
               tokens whose top-2 gap is below TIE_GAP the oracle adopts the
               GPU's choice before slots are recomputed.
+    order:    priority order of the tokens (priority_order), None = token order.
     """
     logits, expert, gap, s, p = gate(x, wg)
     if forced is not None:
@@ -149,7 +224,7 @@ def route(x: np.ndarray, wg: np.ndarray, cap: int, forced=None, override=None) -
         expert = expert.copy()
         expert[np.asarray(idx, dtype=np.int64)] = np.asarray(ex, dtype=np.int32)
     p = s[np.arange(s.shape[0]), expert]
-    slot, count, load = assign_slots(expert, wg.shape[1], cap)
+    slot, count, load = assign_slots(expert, wg.shape[1], cap, order)
     return Routing(logits, expert, gap, s, p, slot, count, load, cap)
 
 
@@ -177,8 +252,8 @@ def forward_group(x, wg, w1, w2, r: Routing):
     return y, cache
 
 
-def backward_group(x, dy, wg, w1, w2, r: Routing, cache):
-    """Backward of forward_group (reading R6, R13).
+def backward_group(x, dy, wg, w1, w2, r: Routing, cache, aux_coef: float = 0.0):
+    """Backward of forward_group (reading R6, R13; aux_coef > 0: reading R21).
 
     do = p dy; dp = <dy, o>; da = do W2_e; dh = da * gelu'(h);
     dx_t = dh W1_e + sum_j dl_tj Wg[:, j], dl_tj = dp_t p_t (delta_{j,e*} - s_tj);
@@ -202,34 +277,41 @@ def backward_group(x, dy, wg, w1, w2, r: Routing, cache):
         onehot = np.zeros((idx.size, E))
         onehot[np.arange(idx.size), e] = 1.0
         dl[idx] = (dp * r.p[idx])[:, None] * (onehot - r.s[idx])
+    if aux_coef:
+        dl = dl + aux_loss_dlogits(r.expert, r.s, aux_coef)
     dx += dl @ wg.T
     dwg = x.T @ dl
     return dx, dwg, dw1, dw2
 
 
-def layer(xs, dys, wg, w1, w2, cf: float, g_tensor: int = 1, forced=None, overrides=None):
+def layer(xs, dys, wg, w1, w2, cf: float, g_tensor: int = 1, forced=None, overrides=None,
+          priority_seed=None, aux_coef: float = 0.0):
     """The whole layer over S token groups, as one process (no communication).
 
     xs, dys: lists of S arrays [T,H] (float64). Each group routes its own T
     tokens with its own capacity C (reading R2). Expert weights are global;
     dW1/dW2 sum over every group's tokens (one EP group, G^e_data = 1).
     forced / overrides: per-group lists (or None).
-    Returns dict with per-group lists 'y', 'dx', 'dwg', 'routing' and summed 'dw1', 'dw2'.
+    priority_seed: random token-selection priority (R20), same seed for every group.
+    aux_coef: auxiliary load-balancing loss coefficient (R21), per group.
+    Returns dict with per-group lists 'y', 'dx', 'dwg', 'routing', 'aux' and summed 'dw1', 'dw2'.
     """
     E = wg.shape[1]
     T = xs[0].shape[0]
     cap = capacity(T, E, cf, g_tensor)
-    out = {"y": [], "dx": [], "dwg": [], "routing": [], "cap": cap,
+    out = {"y": [], "dx": [], "dwg": [], "routing": [], "aux": [], "cap": cap,
            "dw1": np.zeros_like(w1), "dw2": np.zeros_like(w2)}
+    order = None if priority_seed is None else priority_order(T, priority_seed)
     for s, x in enumerate(xs):
         r = route(x, wg, cap,
                   forced=None if forced is None else forced[s],
-                  override=None if overrides is None else overrides[s])
+                  override=None if overrides is None else overrides[s], order=order)
         y, cache = forward_group(x, wg, w1, w2, r)
         out["y"].append(y)
         out["routing"].append(r)
+        out["aux"].append(aux_loss(r.expert, r.s, aux_coef))
         if dys is not None:
-            dx, dwg, dw1, dw2 = backward_group(x, dys[s], wg, w1, w2, r, cache)
+            dx, dwg, dw1, dw2 = backward_group(x, dys[s], wg, w1, w2, r, cache, aux_coef)
             out["dx"].append(dx)
             out["dwg"].append(dwg)
             out["dw1"] += dw1

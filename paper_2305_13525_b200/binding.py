@@ -22,6 +22,8 @@ MOE_F_TIMING = 4
 MOE_F_NCCL_EXCHANGE = 8
 MOE_F_CHECKPOINT = 16
 MOE_F_CAC = 32
+MOE_F_RANDOM_PRIORITY = 64
+MOE_F_AUX_LOSS = 128
 KERNEL_CLASSES = ("route", "dispatch", "gemm", "combine", "combine_bwd", "gate_bwd", "comm")
 COLL_NAMES = ("a2a", "allgather", "reducescatter", "allreduce")
 
@@ -38,7 +40,7 @@ class _Config(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
                 ("experts", ctypes.c_int32), ("capacity_factor", ctypes.c_float),
                 ("g_tensor", ctypes.c_int32), ("g_expert", ctypes.c_int32), ("dtd", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("aux_loss_coef", ctypes.c_float)]
 
 
 class _Layout(ctypes.Structure):
@@ -72,7 +74,7 @@ class _AdamW(ctypes.Structure):
 EXPORTS = ("moe_plan_layout", "moe_plan_bytes", "moe_plan_collectives", "moe_get_unique_id",
            "moe_create", "moe_forward", "moe_backward", "moe_forward_replay", "moe_routing", "moe_stats_get",
            "moe_stats_reset", "moe_destroy", "moe_status_string", "moe_last_error_detail",
-           "moe_gemm_bf16", "moe_adamw_plan", "moe_adamw_step")
+           "moe_gemm_bf16", "moe_adamw_plan", "moe_adamw_step", "moe_aux_loss", "moe_set_priority_seed")
 
 _lib = None
 
@@ -105,6 +107,8 @@ def lib() -> ctypes.CDLL:
     L.moe_last_error_detail.restype = ctypes.c_char_p
     L.moe_gemm_bf16.argtypes = [I, I, I, I, P, I, P, I, P, I, P, I, P]
     I64 = ctypes.c_int64
+    L.moe_aux_loss.argtypes = [P, P, P, P]
+    L.moe_set_priority_seed.argtypes = [P, ctypes.c_uint64]
     L.moe_adamw_plan.argtypes = [I64, I64, ctypes.POINTER(I64), ctypes.POINTER(SZ)]
     L.moe_adamw_step.argtypes = [P, P, P, P, P, I64, ctypes.POINTER(_AdamW), I64, P, P]
     for name in EXPORTS:
@@ -131,10 +135,11 @@ class MoEConfig:
     g_expert: int = 1
     dtd: bool = True
     flags: int = MOE_F_STATS
+    aux_loss_coef: float = 0.0
 
     def c(self) -> _Config:
         return _Config(self.tokens, self.hidden, self.ffn, self.experts, self.capacity_factor,
-                       self.g_tensor, self.g_expert, int(self.dtd), self.flags)
+                       self.g_tensor, self.g_expert, int(self.dtd), self.flags, self.aux_loss_coef)
 
     @staticmethod
     def from_shape(shape, dtd: bool = True, forced: bool = False, tokens: int | None = None):
@@ -270,6 +275,16 @@ class MoELayer:
         _check(lib().moe_routing(self.ctx, _ptr(saved), _ptr(out["expert"]), _ptr(out["slot"]),
                                  _ptr(out["prob"]), _ptr(out["gap"]), _ptr(out["count"]), _stream(stream)))
         return out
+
+    def moe_aux_loss(self, saved, stream=None) -> torch.Tensor:
+        """MOE_F_AUX_LOSS: this forward's l_aux as a 1-element fp32 device tensor."""
+        out = torch.empty(1, dtype=torch.float32, device=self.device)
+        _check(lib().moe_aux_loss(self.ctx, _ptr(saved), _ptr(out), _stream(stream)))
+        return out
+
+    def moe_set_priority_seed(self, seed: int):
+        """MOE_F_RANDOM_PRIORITY: key of the priority permutation for later forwards."""
+        _check(lib().moe_set_priority_seed(self.ctx, seed & ((1 << 64) - 1)))
 
     def moe_stats(self) -> dict:
         s = _Stats()

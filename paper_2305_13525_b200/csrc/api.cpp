@@ -37,6 +37,7 @@ struct moe_ctx {
   size_t scratch_bytes = 0;
   ncclComm_t world_comm = nullptr, tp_comm = nullptr, ep_comm = nullptr;
   bool poisoned = false;
+  uint64_t priority_seed = 0;  // MOE_F_RANDOM_PRIORITY key (moe_set_priority_seed)
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
@@ -754,8 +755,13 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   ra.local_rank = at<int32_t>(c->scratch, sc.local_rank);
   ra.block_hist = at<int32_t>(c->scratch, sc.block_hist);
   ra.ties = at<int32_t>(saved, sv.ties);
+  ra.rts = d.rts ? 1 : 0;
+  ra.seed = c->priority_seed;
+  ra.aux_coef = d.aux_coef;
+  ra.aux_partial = d.aux ? at<float>(c->scratch, sc.auxp) : nullptr;
+  ra.aux_out = d.aux ? at<float>(saved, sv.aux) : nullptr;
   {
-    Scope sc_(c, MOE_K_ROUTE, st, 3);
+    Scope sc_(c, MOE_K_ROUTE, st, d.aux ? 5 : 3);
     CUDA_TRY(c, route(ra, st));
   }
 
@@ -891,7 +897,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     Scope sc_(c, MOE_K_GATE_BWD, st, 4);
     CUDA_TRY(c, gate_bwd(x, dS, wg, logits, expert, slot, prob, dp, ss, d.T, dx, dwg,
                          at<float>(c->scratch, sc.dl), at<float>(c->scratch, sc.dwgp), sc.nsplit,
-                         at<uint8_t>(c->scratch, sc.wpk), st));
+                         at<uint8_t>(c->scratch, sc.wpk),
+                         d.aux ? at<const float>(saved, sv.aux) : nullptr, d.aux_coef, st));
   }
   c->last_stream = st;
   return MOE_OK;
@@ -946,6 +953,21 @@ moe_status moe_routing(moe_ctx* c, const void* saved, int32_t* expert, int32_t* 
   TRY(cp(prob, sv.prob, (size_t)d.T * 4));
   TRY(cp(gap, sv.gap, (size_t)d.T * 4));
   TRY(cp(count, sv.count, (size_t)d.E * 4));
+  return MOE_OK;
+}
+
+moe_status moe_aux_loss(moe_ctx* c, const void* saved, float* aux, void* stream) {
+  if (!c || !saved || !aux) return fail(MOE_ERR_ARG, "null ctx/saved/output");
+  if (!c->d.aux) return fail(MOE_ERR_STATE, "MOE_F_AUX_LOSS not set");
+  if (!c->saved_written.count(saved)) return fail(MOE_ERR_STATE, "saved blob not written by this ctx");
+  CUDA_TRY(c, cudaMemcpyAsync(aux, at<uint8_t>(saved, c->sv.aux + 4 * (size_t)c->d.E), 4,
+                              cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return MOE_OK;
+}
+
+moe_status moe_set_priority_seed(moe_ctx* c, uint64_t seed) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  c->priority_seed = seed;
   return MOE_OK;
 }
 

@@ -59,9 +59,11 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
                            const float* __restrict__ logits, const int32_t* __restrict__ expert,
                            const int32_t* __restrict__ slot, const float* __restrict__ prob,
                            const float* __restrict__ dp, SlotSpace ss, int64_t T,
-                           bf16* __restrict__ dx, float* __restrict__ dl_out) {
+                           bf16* __restrict__ dx, float* __restrict__ dl_out,
+                           const float* __restrict__ aux_f, float aux_scale) {
   constexpr int KK = EPK / 16;  // k-steps per block of A'
   constexpr int KS = 3 * KK;
+  const bool aux = aux_f != nullptr;  // + d l_aux / d l for every token (R21)
   __shared__ __align__(16) float stage[DX_WARPS][16][64 + 4];
   extern __shared__ __align__(16) uint32_t wsm[];  // this CTA's B' fragments
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -93,21 +95,29 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
     for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
       for (int q = 0; q < 4; ++q) dlv[kk][q] = 0.f;
-    if (s >= 0) {
+    if (t < T && (s >= 0 || aux)) {
       const int e = expert[t];
       const float* lg = logits + (size_t)t * E;
       float m = -3.402823e38f;
       for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
       float den = 0.f;
       for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
-      const float gsc = dp[t] * prob[t];
+      const float gsc = s >= 0 ? dp[t] * prob[t] : 0.f;
       const float inv = 1.f / den;
+      float fs = 0.f;  // sum_e f_e s_te
+      if (aux)
+        for (int j = 0; j < E; ++j) fs += aux_f[j] * (expf(lg[j] - m) * inv);
 #pragma unroll
       for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
-          if (j < E) dlv[kk][q] = gsc * ((j == e ? 1.f : 0.f) - expf(lg[j] - m) * inv);
+          if (j < E) {
+            const float sj = expf(lg[j] - m) * inv;
+            float v = gsc * ((j == e ? 1.f : 0.f) - sj);
+            if (aux) v += aux_scale * sj * (aux_f[j] - fs);
+            dlv[kk][q] = v;
+          }
         }
     }
     if (t < T && blockIdx.y == 0) {
@@ -193,6 +203,9 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
         const float2 s2 = unpack_bf16x2(dsv[k].z), s3 = unpack_bf16x2(dsv[k].w);
         o = make_uint4(pack_bf16x2(s0.x + g0.x, s0.y + g0.y), pack_bf16x2(s1.x + g0.z, s1.y + g0.w),
                        pack_bf16x2(s2.x + g1.x, s2.y + g1.y), pack_bf16x2(s3.x + g1.z, s3.y + g1.w));
+      } else if (aux) {  // dropped token: only the aux-loss gate gradient
+        o = make_uint4(pack_bf16x2(g0.x, g0.y), pack_bf16x2(g0.z, g0.w), pack_bf16x2(g1.x, g1.y),
+                       pack_bf16x2(g1.z, g1.w));
       }
       st_v4(dx + (size_t)(t0 + r) * H + h, o);
     }
@@ -341,7 +354,7 @@ template <int EPK, int EP>
 cudaError_t run(const void* x, const void* dS, const float* wg, const float* logits,
                 const int32_t* expert, const int32_t* slot, const float* prob, const float* dp,
                 const SlotSpace& ss, int64_t T, void* dx, float* dwg, float* dl, float* partial,
-                int nsplit, uint32_t* wpk, cudaStream_t s) {
+                int nsplit, uint32_t* wpk, const float* aux_f, float aux_scale, cudaStream_t s) {
   const int H = ss.H, E = ss.E;
   const int KS = 3 * EPK / 16;
   const int64_t npack = (int64_t)(H / 8) * KS * 32;
@@ -369,7 +382,7 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   if (gx > cap) gx = cap;
   gate_bwd_dx_mma_kernel<EPK><<<dim3((unsigned)gx, hsplit), DX_WARPS * 32, smem, s>>>(
       static_cast<const bf16*>(dS), wpk, logits, expert, slot, prob, dp, ss, T,
-      static_cast<bf16*>(dx), dl);
+      static_cast<bf16*>(dx), dl, aux_f, aux_scale);
   constexpr int NT = EP <= 32 ? 4 : 2;
   constexpr int HB = 8 * NT * 8;
   const int64_t tps = ((T + nsplit - 1) / nsplit + DW_TT - 1) / DW_TT * DW_TT;
@@ -391,11 +404,14 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      const int32_t* expert, const int32_t* slot, const float* prob,
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                      float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
-                     cudaStream_t s) {
+                     const float* aux_f, float aux_coef, cudaStream_t s) {
   if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * ss.H * ss.E, s);
   uint32_t* wpk = static_cast<uint32_t*>(pack_scratch);
+  // d l_aux / d l_tj = coef * E / T * s_tj (f_j - sum_e f_e s_te)
+  const float aux_scale = aux_f ? (float)((double)aux_coef * ss.E / (double)T) : 0.f;
 #define RUN(EPK, EP) \
-  run<EPK, EP>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, wpk, s)
+  run<EPK, EP>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, wpk, \
+               aux_f, aux_scale, s)
   if (ss.E <= 8) return RUN(16, 8);  // EP >= 8: a lo row sits in the same thread as its hi row
   if (ss.E <= 16) return RUN(16, 16);
   if (ss.E <= 32) return RUN(32, 32);

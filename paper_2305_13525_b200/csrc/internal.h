@@ -28,6 +28,7 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why);
 cudaError_t gemm_ref(const GemmArgs& a, cudaStream_t s);
 
 // ---- routing / permutation kernels (route.cu, permute.cu) ----
+constexpr int AUX_GRID = 64;  // CTAs of the deterministic P_e reduction (aux loss)
 struct RouteArgs {
   const void* x;        // bf16 [T][H]
   const float* wg;      // [H][E]
@@ -46,6 +47,12 @@ struct RouteArgs {
   int32_t* local_rank;  // scratch [T]
   int32_t* block_hist;  // scratch [ceil(T/1024)][E]
   int32_t* ties;        // [1]: tokens with gap < 1e-6
+  // NEXT #4 gating variants
+  int rts;              // random token-selection priority (R20)
+  uint64_t seed;        //   its permutation key
+  float aux_coef;       // > 0: auxiliary load-balancing loss (R21)
+  float* aux_partial;   //   scratch [AUX_GRID][E]
+  float* aux_out;       //   saved: f_e [E], then l_aux
 };
 cudaError_t route(const RouteArgs& a, cudaStream_t s);
 
@@ -73,11 +80,12 @@ cudaError_t combine_bwd(const void* dy, const void* O, const int32_t* expert, co
 // B10: dx_t = dS[row(t)] + sum_j dl_tj Wg[:, j] (kept), 0 (dropped);
 // dl_tj = dp_t p_t (delta_{j,e*} - softmax(l_t)_j); dWg = sum_t x_t^T dl_t.
 // (gate_bwd.cu) warp-MMA implementation; pack_scratch holds gate_bwd_pack_bytes(H, E).
+// aux_f: f_e [E] of the aux loss (R21) and its coefficient, or null / 0.
 cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float* logits,
                      const int32_t* expert, const int32_t* slot, const float* prob,
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                      float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
-                     cudaStream_t s);
+                     const float* aux_f, float aux_coef, cudaStream_t s);
 int gate_bwd_splits(int64_t T);
 size_t gate_bwd_pack_bytes(int H, int E);
 

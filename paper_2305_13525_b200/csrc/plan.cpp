@@ -27,7 +27,14 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   if (world % tp_ep) { *why = "world % (g_tensor * g_expert) != 0"; return MOE_ERR_SHAPE; }
   if (c->tokens > (int64_t)1 << 30) { *why = "tokens must be < 2^30"; return MOE_ERR_SHAPE; }
   if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING | MOE_F_NCCL_EXCHANGE |
-                   MOE_F_CHECKPOINT | MOE_F_CAC)) { *why = "unknown flag bits"; return MOE_ERR_ARG; }
+                   MOE_F_CHECKPOINT | MOE_F_CAC | MOE_F_RANDOM_PRIORITY | MOE_F_AUX_LOSS)) {
+    *why = "unknown flag bits";
+    return MOE_ERR_ARG;
+  }
+  if ((c->flags & MOE_F_AUX_LOSS) && !(c->aux_loss_coef >= 0.f && std::isfinite(c->aux_loss_coef))) {
+    *why = "aux_loss_coef must be finite and >= 0";
+    return MOE_ERR_ARG;
+  }
   d->T = c->tokens;
   d->H = c->hidden;
   d->F = c->ffn;
@@ -55,6 +62,9 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->peer = world > 1 && (c->flags & MOE_F_NCCL_EXCHANGE) == 0;
   d->ckpt = (c->flags & MOE_F_CHECKPOINT) != 0;
   d->cac = d->ckpt && (c->flags & MOE_F_CAC) != 0;
+  d->rts = (c->flags & MOE_F_RANDOM_PRIORITY) != 0;
+  d->aux = (c->flags & MOE_F_AUX_LOSS) != 0;
+  d->aux_coef = d->aux ? c->aux_loss_coef : 0.f;
   if ((c->flags & MOE_F_CAC) && !d->ckpt) { *why = "MOE_F_CAC needs MOE_F_CHECKPOINT"; return MOE_ERR_ARG; }
   if (d->R > (int64_t)1 << 30) { *why = "rows per expert too large"; return MOE_ERR_SHAPE; }
   return MOE_OK;
@@ -85,6 +95,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sv->load = s.take((size_t)d.E * 4);
   sv->ties = s.take(4);
   sv->tok_of = s.take((size_t)d.E * d.C * 4);
+  sv->aux = d.aux ? s.take((size_t)(d.E + 1) * 4) : 0;  // f_e [E], then l_aux
   // peer mode keeps X and O in the library's ring windows instead of the saved blob,
   // except under checkpointing, where they are the CAC stash; checkpointing keeps G/A
   // out of the saved blob (the replay re-materializes them in scratch)
@@ -103,6 +114,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   Bump f;
   sc->local_rank = f.take((size_t)d.T * 4);
   sc->block_hist = f.take((size_t)((d.T + 1023) / 1024) * d.E * 4);
+  sc->auxp = d.aux ? f.take((size_t)AUX_GRID * d.E * 4) : 0;
   sc->D = (solo || d.peer) ? 0 : f.take(slot_space);  // peer mode dispatches straight into windows
   sc->Ypart = solo ? 0 : f.take(expert_space);
   Bump b;  // backward region reuses the forward region

@@ -25,17 +25,20 @@ struct Dims {
   bool peer;         // world > 1 and the peer-memory exchange (not MOE_F_NCCL_EXCHANGE)
   bool ckpt;         // MOE_F_CHECKPOINT
   bool cac;          // MOE_F_CAC (with ckpt)
+  bool rts;          // MOE_F_RANDOM_PRIORITY
+  bool aux;          // MOE_F_AUX_LOSS
+  float aux_coef;
 };
 
 // Validates and derives; returns MOE_OK or an error with *why set.
 moe_status make_dims(const moe_config* cfg, int world, int rank, Dims* d, std::string* why);
 
 struct SavedLayout {
-  size_t logits, expert, slot, prob, gap, count, load, ties, tok_of, X, G, A, O, total;  // G = gelu'(Hpre)
+  size_t logits, expert, slot, prob, gap, count, load, ties, tok_of, aux, X, G, A, O, total;  // G = gelu'(Hpre)
 };
 struct ScratchLayout {
   // forward
-  size_t local_rank, block_hist, D, Ypart;
+  size_t local_rank, block_hist, auxp, D, Ypart;
   // backward
   size_t dp, dl, dwgp, wpk, dO, dY, dH, dXp, dS;
   // checkpoint mode: G, A re-materialized by the replay (outside both regions)

@@ -193,16 +193,53 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
 constexpr int SCAN_BLOCK = 1024;
 
+// ---------------------------------------------------------------- random priority (R20)
+// sigma(i): token at priority position i. 4-round Feistel network on 2m bits (the
+// smallest 4^m >= T), cycle-walked into [0, T): a bijection of [0, T). Same
+// construction as oracle.priority_order (counter-based; both sides implement it).
+struct Prio {
+  int on, m;
+  uint32_t mask, k[4];
+};
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ uint32_t feistel(uint32_t x, const Prio& p) {
+  uint32_t L = x >> p.m, R = x & p.mask;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t nl = R;
+    R = L ^ (mix32(R ^ p.k[r]) & p.mask);
+    L = nl;
+  }
+  return (L << p.m) | R;
+}
+
+__device__ __forceinline__ int64_t prio_token(int64_t i, int64_t T, const Prio& p) {
+  if (!p.on) return i;
+  uint32_t x = feistel((uint32_t)i, p);
+  while ((int64_t)x >= T) x = feistel(x, p);
+  return x;
+}
+
 // (a) rank of each token among same-expert tokens of its 1024-block + block histogram.
+// Positions i = priority order (token order unless random priority is on).
 __global__ void __launch_bounds__(SCAN_BLOCK)
-    slot_local_kernel(const int32_t* __restrict__ expert, int64_t T, int E,
+    slot_local_kernel(const int32_t* __restrict__ expert, int64_t T, int E, Prio pr,
                       int32_t* __restrict__ local_rank, int32_t* __restrict__ block_hist) {
   __shared__ int32_t wh[32][65];  // per-warp histogram, E <= 64
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
   for (int i = threadIdx.x; i < 32 * 65; i += SCAN_BLOCK) (&wh[0][0])[i] = 0;
   __syncthreads();
-  const int e = (t < T) ? expert[t] : -1;
+  const int e = (t < T) ? expert[prio_token(t, T, pr)] : -1;
   const uint32_t peers = __match_any_sync(0xffffffffu, e);
   const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
   if (e >= 0 && rank_in_warp == 0) wh[warp][e] = __popc(peers);
@@ -225,7 +262,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
 __global__ void __launch_bounds__(SCAN_BLOCK)
     slot_final_kernel(const int32_t* __restrict__ expert, const int32_t* __restrict__ local_rank,
                       const int32_t* __restrict__ block_hist, int64_t T, int E, int64_t C,
-                      int nblocks, int32_t* __restrict__ slot, int32_t* __restrict__ tok_of,
+                      int nblocks, Prio pr, int32_t* __restrict__ slot, int32_t* __restrict__ tok_of,
                       int32_t* __restrict__ count, int32_t* __restrict__ load) {
   __shared__ int32_t prefix[64];
   if (threadIdx.x < E) {
@@ -242,15 +279,81 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
     }
   }
   __syncthreads();
-  const int64_t t = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
-  if (t >= T) return;
+  const int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;  // priority position
+  if (i >= T) return;
+  const int64_t t = prio_token(i, T, pr);
   const int e = expert[t];
-  const int64_t s = (int64_t)prefix[e] + local_rank[t];
+  const int64_t s = (int64_t)prefix[e] + local_rank[i];
   if (s < C) {
     slot[t] = (int32_t)s;
     tok_of[(size_t)e * C + s] = (int32_t)t;
   } else {
     slot[t] = -1;
+  }
+}
+
+// ---------------------------------------------------------------- aux loss (R21)
+// P_e = (1/T) sum_t softmax(l_t)_e: AUX_GRID CTAs over fixed token ranges, each
+// thread sums its tokens in order, then a fixed butterfly per warp and warps in
+// order: deterministic. aux_final: f_e = load_e / T, l_aux = coef E sum_e f_e P_e.
+template <int EMAX>
+__global__ void __launch_bounds__(256)
+    aux_partial_kernel(const float* __restrict__ logits, int64_t T, int E, float* __restrict__ partial) {
+  __shared__ float ws[8][EMAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per = (T + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * per;
+  const int64_t t1 = t0 + per < T ? t0 + per : T;
+  float acc[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) acc[e] = 0.f;
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    float l[EMAX];
+    float m = -FLT_MAX;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      l[e] = e < E ? logits[(size_t)t * E + e] : -FLT_MAX;
+      m = fmaxf(m, l[e]);
+    }
+    float den = 0.f;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      l[e] = e < E ? expf(l[e] - m) : 0.f;
+      den += l[e];
+    }
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) acc[e] += l[e] / den;
+  }
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    const float v = warp_sum(acc[e]);
+    if (lane == 0) ws[warp][e] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < E) {
+    float v = 0.f;
+    for (int w = 0; w < 8; ++w) v += ws[w][threadIdx.x];
+    partial[(size_t)blockIdx.x * E + threadIdx.x] = v;
+  }
+}
+
+__global__ void aux_final_kernel(const float* __restrict__ partial, const int32_t* __restrict__ load,
+                                 int64_t T, int E, float coef, float* __restrict__ out) {
+  __shared__ float fp[64];
+  const int e = threadIdx.x;
+  if (e < E) {
+    float P = 0.f;
+    for (int b = 0; b < AUX_GRID; ++b) P += partial[(size_t)b * E + e];
+    P /= (float)T;
+    const float f = (float)load[e] / (float)T;
+    out[e] = f;
+    fp[e] = f * P;
+  }
+  __syncthreads();
+  if (e == 0) {
+    float sum = 0.f;
+    for (int j = 0; j < E; ++j) sum += fp[j];
+    out[E] = coef * (float)E * sum;
   }
 }
 
@@ -292,6 +395,7 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s) {
   if (a.T == 0) {
     e = cudaMemsetAsync(a.count, 0, sizeof(int32_t) * a.E, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.load, 0, sizeof(int32_t) * a.E, s);
+    if (e == cudaSuccess && a.aux_out) e = cudaMemsetAsync(a.aux_out, 0, sizeof(float) * (a.E + 1), s);
     return e;
   }
   if (a.E <= 4) e = launch_gate<4, 4, 16>(a, s);
@@ -300,10 +404,26 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s) {
   else if (a.E <= 32) e = launch_gate<32, 2, 16>(a, s);
   else e = launch_gate<64, 1, 16>(a, s);
   if (e != cudaSuccess) return e;
+  Prio pr{};
+  if (a.rts) {
+    pr.on = 1;
+    pr.m = 1;
+    while (((int64_t)1 << (2 * pr.m)) < a.T) ++pr.m;
+    pr.mask = (1u << pr.m) - 1u;
+    const uint32_t lo = (uint32_t)a.seed, hi = (uint32_t)(a.seed >> 32);
+    for (int r = 0; r < 4; ++r) pr.k[r] = lo * 0x9E3779B9u + hi + (uint32_t)r * 0x85EBCA6Bu;
+  }
   const int nblocks = (int)((a.T + SCAN_BLOCK - 1) / SCAN_BLOCK);
-  slot_local_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.T, a.E, a.local_rank, a.block_hist);
+  slot_local_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.T, a.E, pr, a.local_rank, a.block_hist);
   slot_final_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.local_rank, a.block_hist, a.T, a.E,
-                                                   a.C, nblocks, a.slot, a.tok_of, a.count, a.load);
+                                                   a.C, nblocks, pr, a.slot, a.tok_of, a.count, a.load);
+  if (a.aux_out) {
+    if (a.E <= 8) aux_partial_kernel<8><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
+    else if (a.E <= 16) aux_partial_kernel<16><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
+    else if (a.E <= 32) aux_partial_kernel<32><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
+    else aux_partial_kernel<64><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
+    aux_final_kernel<<<1, 64, 0, s>>>(a.aux_partial, a.load, a.T, a.E, a.aux_coef, a.aux_out);
+  }
   return cudaGetLastError();
 }
 

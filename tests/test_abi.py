@@ -51,7 +51,8 @@ def test_status_strings():
     (dict(experts=65), "MOE_ERR_SHAPE"),                      # E <= 64
     (dict(tokens=0), "MOE_ERR_ARG"),
     (dict(capacity_factor=0.0), "MOE_ERR_ARG"),
-    (dict(flags=64), "MOE_ERR_ARG"),
+    (dict(flags=256), "MOE_ERR_ARG"),
+    (dict(flags=128, aux_loss_coef=-1.0), "MOE_ERR_ARG"),
 ])
 def test_config_validation(kw, status):
     base = dict(tokens=16384, hidden=2048, ffn=8192, experts=16)
