@@ -101,6 +101,11 @@ typedef struct {
   int32_t dtd;             /* 0 = vanilla (AllReduce + full all-to-all), 1 = DTD       */
   uint32_t flags;          /* MOE_F_*                                                  */
   float aux_loss_coef;     /* MOE_F_AUX_LOSS coefficient (>= 0; ignored without the flag) */
+  int32_t top_k;           /* experts per token: 0 or 1 = top-1 (R1), 2 = top-2 (DESIGN.md
+                              R22: GShard renormalised weights, C = ceil(cf*2T/E), second
+                              choices queue behind all first choices); top-2 needs
+                              experts >= 2 and no MOE_F_FORCED_ROUTING. With top-2 the
+                              per-token routing arrays become [T][2] (expert, slot, prob)  */
 } moe_config;
 
 /* Per-rank derived layout (host-only; no GPU needed). */
@@ -149,7 +154,7 @@ typedef struct {
   int64_t calls[MOE_COLL_KINDS];
   int64_t wire_bytes[MOE_COLL_KINDS];
   int64_t forward_calls, backward_calls;
-  int64_t dropped_tokens;  /* last forward: tokens beyond capacity (this group)       */
+  int64_t dropped_tokens;  /* last forward: (token, choice) pairs beyond capacity (this group) */
   int64_t tie_tokens;      /* last forward: top-2 gap < 1e-6 (logged ties)            */
   int32_t nccl_async_error;/* ncclCommGetAsyncError of the last check (0 = none)      */
   int64_t kernel_launches[MOE_K_CLASSES]; /* CUDA kernels this library launched, per class */
@@ -222,8 +227,9 @@ moe_status moe_forward_replay(moe_ctx* ctx, const void* saved, const void* x, co
                               const void* w1, const void* w2, void* stream);
 
 /* Copies the routing record of a saved blob (device -> device, async).
- * expert/slot int32 [T] (slot -1 = dropped), prob/gap fp32 [T],
- * count int32 [E] (kept per expert, <= C). Any output may be NULL. */
+ * expert/slot int32 [T][K] (slot -1 = dropped), prob fp32 [T][K] (the combine
+ * weights), gap fp32 [T] (top-2: min of the top-1/2 and top-2/3 logit gaps),
+ * count int32 [E] (kept per expert, <= C); K = 1 or top_k. Any output may be NULL. */
 moe_status moe_routing(moe_ctx* ctx, const void* saved, int32_t* expert, int32_t* slot,
                        float* prob, float* gap, int32_t* count, void* stream);
 

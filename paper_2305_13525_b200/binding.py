@@ -40,7 +40,7 @@ class _Config(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
                 ("experts", ctypes.c_int32), ("capacity_factor", ctypes.c_float),
                 ("g_tensor", ctypes.c_int32), ("g_expert", ctypes.c_int32), ("dtd", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("aux_loss_coef", ctypes.c_float)]
+                ("flags", ctypes.c_uint32), ("aux_loss_coef", ctypes.c_float), ("top_k", ctypes.c_int32)]
 
 
 class _Layout(ctypes.Structure):
@@ -136,10 +136,12 @@ class MoEConfig:
     dtd: bool = True
     flags: int = MOE_F_STATS
     aux_loss_coef: float = 0.0
+    top_k: int = 1
 
     def c(self) -> _Config:
         return _Config(self.tokens, self.hidden, self.ffn, self.experts, self.capacity_factor,
-                       self.g_tensor, self.g_expert, int(self.dtd), self.flags, self.aux_loss_coef)
+                       self.g_tensor, self.g_expert, int(self.dtd), self.flags, self.aux_loss_coef,
+                       self.top_k)
 
     @staticmethod
     def from_shape(shape, dtd: bool = True, forced: bool = False, tokens: int | None = None):
@@ -265,11 +267,13 @@ class MoELayer:
                                         _stream(stream)))
 
     def moe_routing(self, saved, stream=None) -> dict:
+        """expert/slot/prob: [T] (top-1) or [T, 2] (top-2); gap [T]; count [E]."""
         T, E = self.cfg.tokens, self.cfg.experts
         dev = self.device
-        out = {"expert": torch.empty(T, dtype=torch.int32, device=dev),
-               "slot": torch.empty(T, dtype=torch.int32, device=dev),
-               "prob": torch.empty(T, dtype=torch.float32, device=dev),
+        shp = (T, 2) if self.cfg.top_k == 2 else (T,)
+        out = {"expert": torch.empty(shp, dtype=torch.int32, device=dev),
+               "slot": torch.empty(shp, dtype=torch.int32, device=dev),
+               "prob": torch.empty(shp, dtype=torch.float32, device=dev),
                "gap": torch.empty(T, dtype=torch.float32, device=dev),
                "count": torch.empty(E, dtype=torch.int32, device=dev)}
         _check(lib().moe_routing(self.ctx, _ptr(saved), _ptr(out["expert"]), _ptr(out["slot"]),

@@ -145,7 +145,7 @@ const T* at(const void* base, size_t off) {
 
 SlotSpace slot_space(const Dims& d) {
   SlotSpace s;
-  s.C = d.C; s.Cs = d.Cs; s.G_t = d.Gt; s.E = d.E; s.H = d.H;
+  s.C = d.C; s.Cs = d.Cs; s.G_t = d.Gt; s.E = d.E; s.H = d.H; s.K = d.K;
   return s;
 }
 
@@ -744,6 +744,7 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   // F1 + F2: gate and capacity slots
   RouteArgs ra;
   ra.x = x; ra.wg = wg; ra.forced = forced_expert; ra.T = d.T; ra.H = d.H; ra.E = d.E; ra.C = d.C;
+  ra.K = d.K;
   ra.logits = at<float>(saved, sv.logits);
   ra.expert = at<int32_t>(saved, sv.expert);
   ra.prob = at<float>(saved, sv.prob);
@@ -948,9 +949,9 @@ moe_status moe_routing(moe_ctx* c, const void* saved, int32_t* expert, int32_t* 
     CUDA_TRY(c, cudaMemcpyAsync(dst, at<uint8_t>(saved, off), bytes, cudaMemcpyDeviceToDevice, st));
     return MOE_OK;
   };
-  TRY(cp(expert, sv.expert, (size_t)d.T * 4));
-  TRY(cp(slot, sv.slot, (size_t)d.T * 4));
-  TRY(cp(prob, sv.prob, (size_t)d.T * 4));
+  TRY(cp(expert, sv.expert, (size_t)d.T * d.K * 4));
+  TRY(cp(slot, sv.slot, (size_t)d.T * d.K * 4));
+  TRY(cp(prob, sv.prob, (size_t)d.T * d.K * 4));
   TRY(cp(gap, sv.gap, (size_t)d.T * 4));
   TRY(cp(count, sv.count, (size_t)d.E * 4));
   return MOE_OK;
@@ -983,7 +984,7 @@ moe_status moe_stats_get(moe_ctx* c, moe_stats* out) {
     int64_t kept = 0;
     for (int32_t v : count) kept += v;
     c->stats.tie_tokens = ties;
-    c->stats.dropped_tokens = c->d.T - kept;
+    c->stats.dropped_tokens = c->d.T * c->d.K - kept;  // dropped (token, choice) pairs
   }
   for (auto& sp : c->spans) {
     float ms = 0.f;

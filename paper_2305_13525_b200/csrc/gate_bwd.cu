@@ -52,8 +52,10 @@ __global__ void wg_pack_kernel(const float* __restrict__ wg, int H, int E, int E
 // dWg, then walks H in 64-wide chunks: 8 n-tiles x KS MMAs, the fp32 results are
 // staged in a per-warp shared tile [16][64] and re-read as 16-byte row pieces so
 // dS[row(t)] is added and dx stored with coalesced 16-byte accesses.
+// KC = 2 (top-2, R22): two dS rows per token and the gate gradient through the
+// renormalised weights w_k = s_ek / (s_e1 + s_e2).
 constexpr int DX_WARPS = 4;
-template <int EPK>
+template <int EPK, int KC>
 __global__ void __launch_bounds__(DX_WARPS * 32)
     gate_bwd_dx_mma_kernel(const bf16* __restrict__ dS, const uint32_t* __restrict__ wpk,
                            const float* __restrict__ logits, const int32_t* __restrict__ expert,
@@ -89,13 +91,41 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int64_t t = t0 + g + 8 * half;
-    const int s = t < T ? slot[t] : -1;
+    const int s = t < T ? slot[t * KC] : -1;
     float dlv[KK][4];  // j = 16 kk + 2 tig + {0, 1, 8, 9}
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
       for (int q = 0; q < 4; ++q) dlv[kk][q] = 0.f;
-    if (t < T && (s >= 0 || aux)) {
+    if (KC == 2 && t < T) {
+      // dL/ds_e1 = s2 (dw1 - dw2) / S^2, dL/ds_e2 = s1 (dw2 - dw1) / S^2 (dw = dp, 0 if dropped)
+      const int e1 = expert[2 * t], e2 = expert[2 * t + 1];
+      const float* lg = logits + (size_t)t * E;
+      float m = -3.402823e38f;
+      for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
+      float den = 0.f;
+      for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
+      const float inv = 1.f / den;
+      const float s1 = expf(lg[e1] - m) * inv, s2 = expf(lg[e2] - m) * inv;
+      const float S = s1 + s2, dw1 = dp[2 * t], dw2 = dp[2 * t + 1];
+      const float c1 = s1 * s2 * (dw1 - dw2) / (S * S);  // g1 * s1
+      const float c2 = s2 * s1 * (dw2 - dw1) / (S * S);  // g2 * s2
+      float fs = 0.f;
+      if (aux)
+        for (int j = 0; j < E; ++j) fs += aux_f[j] * (expf(lg[j] - m) * inv);
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
+          if (j < E) {
+            const float sj = expf(lg[j] - m) * inv;
+            float v = c1 * ((j == e1 ? 1.f : 0.f) - sj) + c2 * ((j == e2 ? 1.f : 0.f) - sj);
+            if (aux) v += aux_scale * sj * (aux_f[j] - fs);
+            dlv[kk][q] = v;
+          }
+        }
+    } else if (KC == 1 && t < T && (s >= 0 || aux)) {
       const int e = expert[t];
       const float* lg = logits + (size_t)t * E;
       float m = -3.402823e38f;
@@ -144,34 +174,41 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
   }
   // per-lane row pieces for the coalesced pass: piece p = lane + 32 k (k < 4) of the
   // 16 x 64 tile -> row p / 8, 8 columns at 8 * (p % 8)
-  size_t rowoff[4];
-  bool kept[4], valid[4];
+  size_t rowoff[4][KC];
+  bool kept[4][KC], valid[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int r = (lane + 32 * k) >> 3;
     const int64_t t = t0 + r;
     valid[k] = t < T;
-    const int s = valid[k] ? slot[t] : -1;
-    kept[k] = s >= 0;
-    rowoff[k] = kept[k] ? slot_row2(ss, expert[t], s) : 0;
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      const int s = valid[k] ? slot[t * KC + c] : -1;
+      kept[k][c] = s >= 0;
+      rowoff[k][c] = kept[k][c] ? slot_row2(ss, expert[t * KC + c], s) : 0;
+    }
   }
 
   const int ntiles = nt_end;
-  auto load_ds = [&](int n0, uint4 (&dsv)[4]) {
+  auto load_ds = [&](int n0, uint4 (&dsv)[4][KC]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int c = 8 * ((lane + 32 * k) & 7);
       const int h = 8 * n0 + c;
-      dsv[k] = (kept[k] && n0 < ntiles && h < 8 * ntiles) ? ld_nc_v4(dS + rowoff[k] + h)
-                                                           : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < KC; ++q)
+        dsv[k][q] = (kept[k][q] && n0 < ntiles && h < 8 * ntiles) ? ld_nc_v4(dS + rowoff[k][q] + h)
+                                                                   : make_uint4(0, 0, 0, 0);
     }
   };
-  uint4 dsn[4];
+  uint4 dsn[4][KC];
   load_ds(nt_begin, dsn);
   for (int n0 = nt_begin; n0 < ntiles; n0 += 8) {
-    uint4 dsv[4];
+    uint4 dsv[4][KC];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) dsv[k] = dsn[k];
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < KC; ++q) dsv[k][q] = dsn[k][q];
     load_ds(n0 + 8, dsn);  // next chunk's dS in flight during this chunk's MMAs
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -198,9 +235,21 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
       const float4 g0 = *reinterpret_cast<const float4*>(&stage[warp][r][c]);
       const float4 g1 = *reinterpret_cast<const float4*>(&stage[warp][r][c + 4]);
       uint4 o = make_uint4(0, 0, 0, 0);
-      if (kept[k]) {
-        const float2 s0 = unpack_bf16x2(dsv[k].x), s1 = unpack_bf16x2(dsv[k].y);
-        const float2 s2 = unpack_bf16x2(dsv[k].z), s3 = unpack_bf16x2(dsv[k].w);
+      if (KC == 2) {  // dS rows of the kept choices (zeros otherwise) + the gate term
+        float sv[8];
+        const uint32_t a0[4] = {dsv[k][0].x, dsv[k][0].y, dsv[k][0].z, dsv[k][0].w};
+        const uint32_t a1[4] = {dsv[k][KC - 1].x, dsv[k][KC - 1].y, dsv[k][KC - 1].z, dsv[k][KC - 1].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 u0 = unpack_bf16x2(a0[q]), u1 = unpack_bf16x2(a1[q]);
+          sv[2 * q] = u0.x + u1.x;
+          sv[2 * q + 1] = u0.y + u1.y;
+        }
+        o = make_uint4(pack_bf16x2(sv[0] + g0.x, sv[1] + g0.y), pack_bf16x2(sv[2] + g0.z, sv[3] + g0.w),
+                       pack_bf16x2(sv[4] + g1.x, sv[5] + g1.y), pack_bf16x2(sv[6] + g1.z, sv[7] + g1.w));
+      } else if (kept[k][0]) {
+        const float2 s0 = unpack_bf16x2(dsv[k][0].x), s1 = unpack_bf16x2(dsv[k][0].y);
+        const float2 s2 = unpack_bf16x2(dsv[k][0].z), s3 = unpack_bf16x2(dsv[k][0].w);
         o = make_uint4(pack_bf16x2(s0.x + g0.x, s0.y + g0.y), pack_bf16x2(s1.x + g0.z, s1.y + g0.w),
                        pack_bf16x2(s2.x + g1.x, s2.y + g1.y), pack_bf16x2(s3.x + g1.z, s3.y + g1.w));
       } else if (aux) {  // dropped token: only the aux-loss gate gradient
@@ -350,7 +399,7 @@ __global__ void dwg_reduce2_kernel(const float* __restrict__ partial, int nsplit
   dwg[i] = s;
 }
 
-template <int EPK, int EP>
+template <int EPK, int EP, int KC>
 cudaError_t run(const void* x, const void* dS, const float* wg, const float* logits,
                 const int32_t* expert, const int32_t* slot, const float* prob, const float* dp,
                 const SlotSpace& ss, int64_t T, void* dx, float* dwg, float* dl, float* partial,
@@ -369,7 +418,7 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   const size_t smem = slice_bytes(hsplit);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_mma_kernel<EPK>,
+    cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_mma_kernel<EPK, KC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -380,7 +429,7 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   int64_t gx = (T + tb - 1) / tb;
   const int64_t cap = (3 * (int64_t)sms + hsplit - 1) / hsplit;  // ~3 CTAs per SM, persistent
   if (gx > cap) gx = cap;
-  gate_bwd_dx_mma_kernel<EPK><<<dim3((unsigned)gx, hsplit), DX_WARPS * 32, smem, s>>>(
+  gate_bwd_dx_mma_kernel<EPK, KC><<<dim3((unsigned)gx, hsplit), DX_WARPS * 32, smem, s>>>(
       static_cast<const bf16*>(dS), wpk, logits, expert, slot, prob, dp, ss, T,
       static_cast<bf16*>(dx), dl, aux_f, aux_scale);
   constexpr int NT = EP <= 32 ? 4 : 2;
@@ -409,9 +458,11 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
   uint32_t* wpk = static_cast<uint32_t*>(pack_scratch);
   // d l_aux / d l_tj = coef * E / T * s_tj (f_j - sum_e f_e s_te)
   const float aux_scale = aux_f ? (float)((double)aux_coef * ss.E / (double)T) : 0.f;
-#define RUN(EPK, EP) \
-  run<EPK, EP>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, dwg_partial, nsplit, wpk, \
-               aux_f, aux_scale, s)
+#define RUN(EPK, EP)                                                                                         \
+  (ss.K == 2 ? run<EPK, EP, 2>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch,        \
+                               dwg_partial, nsplit, wpk, aux_f, aux_scale, s)                                 \
+             : run<EPK, EP, 1>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch,        \
+                               dwg_partial, nsplit, wpk, aux_f, aux_scale, s))
   if (ss.E <= 8) return RUN(16, 8);  // EP >= 8: a lo row sits in the same thread as its hi row
   if (ss.E <= 16) return RUN(16, 16);
   if (ss.E <= 32) return RUN(32, 32);

@@ -35,23 +35,24 @@ struct RouteArgs {
   const int32_t* forced;  // [T] or null
   int64_t T;
   int H, E;
+  int K;                // experts per token (1, or 2 for top-2, R22)
   int64_t C;
   float* logits;        // [T][E]
-  int32_t* expert;      // [T]
-  float* prob;          // [T]
+  int32_t* expert;      // [T][K]
+  float* prob;          // [T][K] combine weights
   float* gap;           // [T]
-  int32_t* slot;        // [T]
+  int32_t* slot;        // [T][K]
   int32_t* count;       // [E]   kept per expert
   int32_t* load;        // [E]   routed per expert (pre-capacity)
-  int32_t* tok_of;      // [E][C] token of (expert, slot), valid for slot < count
-  int32_t* local_rank;  // scratch [T]
-  int32_t* block_hist;  // scratch [ceil(T/1024)][E]
+  int32_t* tok_of;      // [E][C] item (token * K + choice) of (expert, slot), valid for slot < count
+  int32_t* local_rank;  // scratch [K*T]
+  int32_t* block_hist;  // scratch [ceil(K*T/1024)][E]
   int32_t* ties;        // [1]: tokens with gap < 1e-6
   // NEXT #4 gating variants
   int rts;              // random token-selection priority (R20)
   uint64_t seed;        //   its permutation key
   float aux_coef;       // > 0: auxiliary load-balancing loss (R21)
-  float* aux_partial;   //   scratch [AUX_GRID][E]
+  float* aux_partial;   //   scratch [AUX_GRID][E] fp32 + [AUX_GRID][E] int32
   float* aux_out;       //   saved: f_e [E], then l_aux
 };
 cudaError_t route(const RouteArgs& a, cudaStream_t s);
@@ -60,6 +61,7 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s);
 struct SlotSpace {
   int64_t C, Cs;  // capacity and slot-slice size
   int G_t, E, H;
+  int K = 1;      // choices per token: per-token arrays are [T][K], tok_of holds token*K+choice
 };
 
 // F3: D[tt][e][cs] = x[tok_of[e][tt*Cs+cs]] (zeros for empty slots), for slices
@@ -67,12 +69,12 @@ struct SlotSpace {
 cudaError_t dispatch(const void* x, const int32_t* tok_of, const int32_t* count,
                      const SlotSpace& ss, int t_lo, int t_hi, void* D, cudaStream_t s);
 
-// F11: y_t = bf16(p_t * O[row(t)]), 0 if dropped.
+// F11: y_t = bf16(sum over kept choices k of p_tk * O[row(t,k)]), 0 if all dropped.
 cudaError_t combine(const void* O, const int32_t* expert, const int32_t* slot, const float* prob,
                     const SlotSpace& ss, int64_t T, void* y, cudaStream_t s);
 
-// B1: dp_t = <dy_t, O[row(t)]> (fp32), dO[row(t)] = bf16(p_t dy_t) for kept
-// tokens whose slot lies in slices [t_lo, t_hi); empty slots in those slices -> 0.
+// B1: dp_tk = <dy_t, O[row(t,k)]> (fp32, 0 if dropped), dO[row(t,k)] = bf16(p_tk dy_t) for
+// kept choices whose slot lies in slices [t_lo, t_hi); empty slots in those slices -> 0.
 cudaError_t combine_bwd(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
                         const float* prob, const int32_t* count, const SlotSpace& ss, int64_t T,
                         int t_lo, int t_hi, float* dp, void* dO, cudaStream_t s);

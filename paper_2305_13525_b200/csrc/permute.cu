@@ -1,7 +1,7 @@
 // permute.cu — the HBM-bound steps of the hot path:
 //   F3  dispatch      slot-parallel gather x -> capacity-padded slot space
-//   F11 combine       token-parallel y_t = p_t * O[row(t)]
-//   B1  combine_bwd   dp_t = <dy_t, O[row(t)]>, dO[row(t)] = p_t dy_t
+//   F11 combine       token-parallel y_t = sum_k p_tk * O[row(t,k)]  (K = 1, or 2 for top-2)
+//   B1  combine_bwd   dp_tk = <dy_t, O[row(t,k)]>, dO[row(t,k)] = p_tk dy_t
 // Slot space is [G_t][E][C_s][H]: slot c of expert e lives in slice c / C_s at
 // row c % C_s, so a DTD rank touches only its own slice.
 // Rows move as 16-byte vectors, one warp per row/token, all loads of a row
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   bf16* dst = D + ((size_t)(tt * ss.E + e) * ss.Cs + cs) * ss.H;
   const int nv = ss.H / 8;
   if (c < count[e]) {
-    const int t = tok_of[(size_t)e * ss.C + c];
+    const int t = tok_of[(size_t)e * ss.C + c] / ss.K;  // item -> token
     copy_row<false>(x + (size_t)t * ss.H, dst, nv, lane);
   } else {
     copy_row<true>(nullptr, dst, nv, lane);
@@ -69,32 +69,47 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (t >= T) return;
-  const int s = slot[t];
+  const int K = ss.K;
   const int nv = ss.H / 8;
   bf16* dst = y + (size_t)t * ss.H;
-  if (s < 0) {
+  const bf16* src[2] = {nullptr, nullptr};
+  float p[2] = {0.f, 0.f};
+  int nk = 0;
+  for (int k = 0; k < K; ++k) {
+    const int s = slot[t * K + k];
+    if (s < 0) continue;
+    src[nk] = O + slot_row(ss, expert[t * K + k], s);
+    p[nk] = prob[t * K + k];
+    ++nk;
+  }
+  if (nk == 0) {
     copy_row<true>(nullptr, dst, nv, lane);
     return;
   }
-  const bf16* src = O + slot_row(ss, expert[t], s);
-  const float p = prob[t];
   constexpr int U = 8;
   for (int v0 = 0; v0 < nv; v0 += 32 * U) {
-    uint4 buf[U];
+    uint4 buf[U], buf2[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int v = v0 + u * 32 + lane;
-      buf[u] = v < nv ? ld_nc_v4(src + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+      buf[u] = v < nv ? ld_nc_v4(src[0] + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+      buf2[u] = (nk > 1 && v < nv) ? ld_nc_v4(src[1] + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int v = v0 + u * 32 + lane;
       if (v < nv) {
         uint32_t w[4] = {buf[u].x, buf[u].y, buf[u].z, buf[u].w};
+        const uint32_t w2[4] = {buf2[u].x, buf2[u].y, buf2[u].z, buf2[u].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          float2 f = unpack_bf16x2(w[k]);
-          w[k] = pack_bf16x2(p * f.x, p * f.y);
+          const float2 f = unpack_bf16x2(w[k]);
+          float2 r = make_float2(p[0] * f.x, p[0] * f.y);
+          if (nk > 1) {  // second choice (top-2): fp32 sum, one rounding
+            const float2 f2 = unpack_bf16x2(w2[k]);
+            r = make_float2(fmaf(p[1], f2.x, r.x), fmaf(p[1], f2.y, r.y));
+          }
+          w[k] = pack_bf16x2(r.x, r.y);
         }
         st_v4(dst + (size_t)v * 8, make_uint4(w[0], w[1], w[2], w[3]));
       }
@@ -110,15 +125,17 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (t >= T) return;
-  const int s = slot[t];
+  for (int kc = 0; kc < ss.K; ++kc) {
+  const int64_t it = t * ss.K + kc;
+  const int s = slot[it];
   if (s < 0) {
-    if (lane == 0) dp[t] = 0.f;
-    return;
+    if (lane == 0) dp[it] = 0.f;
+    continue;
   }
-  const size_t row = slot_row(ss, expert[t], s);
+  const size_t row = slot_row(ss, expert[it], s);
   const int tt = (int)(s / ss.Cs);
   const bool mine = tt >= t_lo && tt < t_hi;
-  const float p = prob[t];
+  const float p = prob[it];
   const bf16* dyr = dy + (size_t)t * ss.H;
   const bf16* orow = O + row;
   bf16* dst = dO + row;
@@ -150,7 +167,8 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
   }
   acc = warp_sum(acc);
-  if (lane == 0) dp[t] = acc;
+  if (lane == 0) dp[it] = acc;
+  }
 }
 
 // zero-fill the empty slots (c >= count[e]) of slices [t_lo, t_hi)
@@ -196,7 +214,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int64_t c = (int64_t)tt * ss.Cs + cs;
   const int nv = ss.H / 8;
   const bool full = c < count[e];
-  const bf16* src = full ? x + (size_t)tok_of[(size_t)e * ss.C + c] * ss.H : nullptr;
+  const bf16* src = full ? x + (size_t)(tok_of[(size_t)e * ss.C + c] / ss.K) * ss.H : nullptr;
   const int nd = pd.dtd ? pd.Gt : 1;
   constexpr int U = 8;
   for (int v0 = 0; v0 < nv; v0 += 32 * U) {
@@ -228,17 +246,19 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (t >= T) return;
-  const int s = slot[t];
+  for (int kc = 0; kc < ss.K; ++kc) {
+  const int64_t it = t * ss.K + kc;
+  const int s = slot[it];
   if (s < 0) {
-    if (lane == 0) dp[t] = 0.f;
-    return;
+    if (lane == 0) dp[it] = 0.f;
+    continue;
   }
-  const int e = expert[t];
+  const int e = expert[it];
   const size_t row = slot_row(ss, e, s);
   const int tt = (int)(s / ss.Cs);
   const int64_t cs = s - (int64_t)tt * ss.Cs;
   const bool mine = tt >= t_lo && tt < t_hi;
-  const float p = prob[t];
+  const float p = prob[it];
   const bf16* dyr = dy + (size_t)t * ss.H;
   const bf16* orow = O + row;
   const int nv = ss.H / 8;
@@ -278,7 +298,8 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
   }
   acc = warp_sum(acc);
-  if (lane == 0) dp[t] = acc;
+  if (lane == 0) dp[it] = acc;
+  }
   __threadfence_system();
 }
 

@@ -35,6 +35,13 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
     *why = "aux_loss_coef must be finite and >= 0";
     return MOE_ERR_ARG;
   }
+  if (c->top_k < 0 || c->top_k > 2) { *why = "top_k must be 0, 1 or 2"; return MOE_ERR_ARG; }
+  if (c->top_k == 2 && c->experts < 2) { *why = "top-2 needs experts >= 2"; return MOE_ERR_SHAPE; }
+  if (c->top_k == 2 && (c->flags & MOE_F_FORCED_ROUTING)) {
+    *why = "forced routing is top-1 only";
+    return MOE_ERR_UNSUPPORTED;
+  }
+  d->K = c->top_k == 2 ? 2 : 1;
   d->T = c->tokens;
   d->H = c->hidden;
   d->F = c->ffn;
@@ -49,8 +56,8 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->d = rank / tp_ep;
   d->El = d->E / d->Gep;
   d->Fl = d->F / d->Gt;
-  // Reading R2: C = ceil(cf*T/E) (double), >= 1, rounded up to a multiple of G_t.
-  int64_t C = (int64_t)std::ceil((double)c->capacity_factor * (double)d->T / (double)d->E);
+  // Reading R2: C = ceil(cf*K*T/E) (double), >= 1, rounded up to a multiple of G_t (R22: K = 2).
+  int64_t C = (int64_t)std::ceil((double)c->capacity_factor * (double)d->K * (double)d->T / (double)d->E);
   if (C < 1) C = 1;
   C = ceil_div(C, d->Gt) * d->Gt;
   d->C = C;
@@ -87,9 +94,9 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   const size_t ffn_space = (size_t)d.El * d.R * d.Fl * 2;           // [E_l][R][F_l]
   Bump s;
   sv->logits = s.take((size_t)d.T * d.E * 4);
-  sv->expert = s.take((size_t)d.T * 4);
-  sv->slot = s.take((size_t)d.T * 4);
-  sv->prob = s.take((size_t)d.T * 4);
+  sv->expert = s.take((size_t)d.T * d.K * 4);
+  sv->slot = s.take((size_t)d.T * d.K * 4);
+  sv->prob = s.take((size_t)d.T * d.K * 4);
   sv->gap = s.take((size_t)d.T * 4);
   sv->count = s.take((size_t)d.E * 4);
   sv->load = s.take((size_t)d.E * 4);
@@ -112,13 +119,13 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dXp_is_dS = solo;
   sc->nsplit = gate_bwd_splits(d.T);
   Bump f;
-  sc->local_rank = f.take((size_t)d.T * 4);
-  sc->block_hist = f.take((size_t)((d.T + 1023) / 1024) * d.E * 4);
-  sc->auxp = d.aux ? f.take((size_t)AUX_GRID * d.E * 4) : 0;
+  sc->local_rank = f.take((size_t)d.T * d.K * 4);
+  sc->block_hist = f.take((size_t)((d.T * d.K + 1023) / 1024) * d.E * 4);
+  sc->auxp = d.aux ? f.take((size_t)AUX_GRID * d.E * 8) : 0;  // P partials + first-choice counts
   sc->D = (solo || d.peer) ? 0 : f.take(slot_space);  // peer mode dispatches straight into windows
   sc->Ypart = solo ? 0 : f.take(expert_space);
   Bump b;  // backward region reuses the forward region
-  sc->dp = b.take((size_t)d.T * 4);
+  sc->dp = b.take((size_t)d.T * d.K * 4);
   sc->dl = b.take((size_t)d.T * d.E * 4);
   sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));

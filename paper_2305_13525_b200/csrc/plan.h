@@ -28,6 +28,7 @@ struct Dims {
   bool rts;          // MOE_F_RANDOM_PRIORITY
   bool aux;          // MOE_F_AUX_LOSS
   float aux_coef;
+  int K;             // experts per token (top_k: 1 or 2)
 };
 
 // Validates and derives; returns MOE_OK or an error with *why set.

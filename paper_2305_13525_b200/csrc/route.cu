@@ -64,7 +64,7 @@ __device__ __forceinline__ void stage_wg_pairs(float* ws, const float* __restric
 template <int EMAX, int TPW, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     gate_kernel(const bf16* __restrict__ x, const float* __restrict__ wg,
-                const int32_t* __restrict__ forced, int64_t T, int H, int E, int hch,
+                const int32_t* __restrict__ forced, int64_t T, int H, int E, int hch, int K,
                 float* __restrict__ logits, int32_t* __restrict__ expert,
                 float* __restrict__ prob, float* __restrict__ gap, int32_t* __restrict__ ties) {
   constexpr int EP = EMAX / 2;
@@ -177,6 +177,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         if (e >= E) break;
         den += expf(lv[e] - m);
       }
+      if (K == 2) {  // R22: second = lowest-index max over e != best; gap over the top 3
+        float v2 = -FLT_MAX, v3 = -FLT_MAX;
+        int e2 = best == 0 ? 1 : 0;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+          if (e >= E) break;
+          if (e == best) continue;
+          const float v = lv[e];
+          if (v > v2) { v3 = v2; v2 = v; e2 = e; }
+          else if (v > v3) { v3 = v; }
+        }
+        const float g = E > 2 ? fminf(m - v2, v2 - v3) : m - v2;
+        const float s1 = 1.f / den, s2 = expf(v2 - m) / den;
+        expert[2 * tok] = best;
+        expert[2 * tok + 1] = e2;
+        prob[2 * tok] = s1 / (s1 + s2);
+        prob[2 * tok + 1] = s2 / (s1 + s2);
+        gap[tok] = g;
+        if (g < 1e-6f) atomicAdd(ties, 1);
+        continue;
+      }
       const int chosen = forced ? forced[tok] : best;
       float lc = m;
 #pragma unroll
@@ -229,17 +250,26 @@ __device__ __forceinline__ int64_t prio_token(int64_t i, int64_t T, const Prio& 
   return x;
 }
 
-// (a) rank of each token among same-expert tokens of its 1024-block + block histogram.
+// Scan items i in [0, K*T): pass k = i / T (first choices, then second choices, R22),
+// priority position q = i % T -> token prio_token(q); the item id t*K + k indexes the
+// per-(token, choice) arrays.
+__device__ __forceinline__ int64_t item_id(int64_t i, int64_t T, int K, const Prio& p) {
+  const int64_t k = K == 1 ? 0 : i / T;
+  return prio_token(i - k * T, T, p) * K + k;
+}
+
+// (a) rank of each item among same-expert items of its 1024-block + block histogram.
 // Positions i = priority order (token order unless random priority is on).
 __global__ void __launch_bounds__(SCAN_BLOCK)
-    slot_local_kernel(const int32_t* __restrict__ expert, int64_t T, int E, Prio pr,
+    slot_local_kernel(const int32_t* __restrict__ expert, int64_t T, int K, int E, Prio pr,
                       int32_t* __restrict__ local_rank, int32_t* __restrict__ block_hist) {
+  const int64_t N = T * K;
   __shared__ int32_t wh[32][65];  // per-warp histogram, E <= 64
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;
   for (int i = threadIdx.x; i < 32 * 65; i += SCAN_BLOCK) (&wh[0][0])[i] = 0;
   __syncthreads();
-  const int e = (t < T) ? expert[prio_token(t, T, pr)] : -1;
+  const int e = (t < N) ? expert[item_id(t, T, K, pr)] : -1;
   const uint32_t peers = __match_any_sync(0xffffffffu, e);
   const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
   if (e >= 0 && rank_in_warp == 0) wh[warp][e] = __popc(peers);
@@ -255,13 +285,13 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
     block_hist[(size_t)blockIdx.x * E + threadIdx.x] = run;
   }
   __syncthreads();
-  if (t < T) local_rank[t] = wh[warp][e] + rank_in_warp;
+  if (t < N) local_rank[t] = wh[warp][e] + rank_in_warp;
 }
 
 // (b) slot = block prefix + local rank; keep iff slot < C; inverse map; counts.
 __global__ void __launch_bounds__(SCAN_BLOCK)
     slot_final_kernel(const int32_t* __restrict__ expert, const int32_t* __restrict__ local_rank,
-                      const int32_t* __restrict__ block_hist, int64_t T, int E, int64_t C,
+                      const int32_t* __restrict__ block_hist, int64_t T, int K, int E, int64_t C,
                       int nblocks, Prio pr, int32_t* __restrict__ slot, int32_t* __restrict__ tok_of,
                       int32_t* __restrict__ count, int32_t* __restrict__ load) {
   __shared__ int32_t prefix[64];
@@ -279,16 +309,16 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
     }
   }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;  // priority position
-  if (i >= T) return;
-  const int64_t t = prio_token(i, T, pr);
-  const int e = expert[t];
+  const int64_t i = (int64_t)blockIdx.x * SCAN_BLOCK + threadIdx.x;  // scan item
+  if (i >= T * K) return;
+  const int64_t it = item_id(i, T, K, pr);
+  const int e = expert[it];
   const int64_t s = (int64_t)prefix[e] + local_rank[i];
   if (s < C) {
-    slot[t] = (int32_t)s;
-    tok_of[(size_t)e * C + s] = (int32_t)t;
+    slot[it] = (int32_t)s;
+    tok_of[(size_t)e * C + s] = (int32_t)it;  // item id: token * K + choice
   } else {
-    slot[t] = -1;
+    slot[it] = -1;
   }
 }
 
@@ -298,8 +328,13 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
 // order: deterministic. aux_final: f_e = load_e / T, l_aux = coef E sum_e f_e P_e.
 template <int EMAX>
 __global__ void __launch_bounds__(256)
-    aux_partial_kernel(const float* __restrict__ logits, int64_t T, int E, float* __restrict__ partial) {
+    aux_partial_kernel(const float* __restrict__ logits, const int32_t* __restrict__ expert, int64_t T,
+                       int K, int E, float* __restrict__ partial) {
   __shared__ float ws[8][EMAX];
+  __shared__ int wc[8][EMAX];
+  int cnt[EMAX];  // first choices (f_e counts only the first choice, R21/R22)
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) cnt[e] = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t per = (T + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * per;
@@ -323,29 +358,40 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int e = 0; e < EMAX; ++e) acc[e] += l[e] / den;
+    const int e1 = expert[(size_t)t * K];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) cnt[e] += e == e1;
   }
 #pragma unroll
   for (int e = 0; e < EMAX; ++e) {
     const float v = warp_sum(acc[e]);
-    if (lane == 0) ws[warp][e] = v;
+    int c = cnt[e];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) { ws[warp][e] = v; wc[warp][e] = c; }
   }
   __syncthreads();
   if (threadIdx.x < E) {
     float v = 0.f;
-    for (int w = 0; w < 8; ++w) v += ws[w][threadIdx.x];
+    int c = 0;
+    for (int w = 0; w < 8; ++w) { v += ws[w][threadIdx.x]; c += wc[w][threadIdx.x]; }
     partial[(size_t)blockIdx.x * E + threadIdx.x] = v;
+    reinterpret_cast<int32_t*>(partial + (size_t)AUX_GRID * E)[(size_t)blockIdx.x * E + threadIdx.x] = c;
   }
 }
 
-__global__ void aux_final_kernel(const float* __restrict__ partial, const int32_t* __restrict__ load,
-                                 int64_t T, int E, float coef, float* __restrict__ out) {
+__global__ void aux_final_kernel(const float* __restrict__ partial, int64_t T, int E, float coef,
+                                 float* __restrict__ out) {
   __shared__ float fp[64];
   const int e = threadIdx.x;
   if (e < E) {
     float P = 0.f;
     for (int b = 0; b < AUX_GRID; ++b) P += partial[(size_t)b * E + e];
     P /= (float)T;
-    const float f = (float)load[e] / (float)T;
+    int64_t n1 = 0;
+    const int32_t* cnt = reinterpret_cast<const int32_t*>(partial + (size_t)AUX_GRID * E);
+    for (int b = 0; b < AUX_GRID; ++b) n1 += cnt[(size_t)b * E + e];
+    const float f = (float)n1 / (float)T;
     out[e] = f;
     fp[e] = f * P;
   }
@@ -382,7 +428,7 @@ cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
   int64_t grid = (a.T + per_cta - 1) / per_cta;
   if (hch >= a.H && grid > g_sms) grid = g_sms;  // Wg resident: persistent over token batches
   gate_kernel<EMAX, TPW, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(
-      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, hch, a.logits, a.expert,
+      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, hch, a.K, a.logits, a.expert,
       a.prob, a.gap, a.ties);
   return cudaGetLastError();
 }
@@ -413,16 +459,16 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s) {
     const uint32_t lo = (uint32_t)a.seed, hi = (uint32_t)(a.seed >> 32);
     for (int r = 0; r < 4; ++r) pr.k[r] = lo * 0x9E3779B9u + hi + (uint32_t)r * 0x85EBCA6Bu;
   }
-  const int nblocks = (int)((a.T + SCAN_BLOCK - 1) / SCAN_BLOCK);
-  slot_local_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.T, a.E, pr, a.local_rank, a.block_hist);
-  slot_final_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.local_rank, a.block_hist, a.T, a.E,
+  const int nblocks = (int)((a.T * a.K + SCAN_BLOCK - 1) / SCAN_BLOCK);
+  slot_local_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.T, a.K, a.E, pr, a.local_rank, a.block_hist);
+  slot_final_kernel<<<nblocks, SCAN_BLOCK, 0, s>>>(a.expert, a.local_rank, a.block_hist, a.T, a.K, a.E,
                                                    a.C, nblocks, pr, a.slot, a.tok_of, a.count, a.load);
   if (a.aux_out) {
-    if (a.E <= 8) aux_partial_kernel<8><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
-    else if (a.E <= 16) aux_partial_kernel<16><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
-    else if (a.E <= 32) aux_partial_kernel<32><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
-    else aux_partial_kernel<64><<<AUX_GRID, 256, 0, s>>>(a.logits, a.T, a.E, a.aux_partial);
-    aux_final_kernel<<<1, 64, 0, s>>>(a.aux_partial, a.load, a.T, a.E, a.aux_coef, a.aux_out);
+    if (a.E <= 8) aux_partial_kernel<8><<<AUX_GRID, 256, 0, s>>>(a.logits, a.expert, a.T, a.K, a.E, a.aux_partial);
+    else if (a.E <= 16) aux_partial_kernel<16><<<AUX_GRID, 256, 0, s>>>(a.logits, a.expert, a.T, a.K, a.E, a.aux_partial);
+    else if (a.E <= 32) aux_partial_kernel<32><<<AUX_GRID, 256, 0, s>>>(a.logits, a.expert, a.T, a.K, a.E, a.aux_partial);
+    else aux_partial_kernel<64><<<AUX_GRID, 256, 0, s>>>(a.logits, a.expert, a.T, a.K, a.E, a.aux_partial);
+    aux_final_kernel<<<1, 64, 0, s>>>(a.aux_partial, a.T, a.E, a.aux_coef, a.aux_out);
   }
   return cudaGetLastError();
 }

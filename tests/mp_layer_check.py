@@ -25,8 +25,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import moe_oracle as O  # noqa: E402
-from paper_2305_13525_b200 import (MOE_F_CAC, MOE_F_CHECKPOINT, MOE_F_NCCL_EXCHANGE, MoEConfig,  # noqa: E402
-                                   MoELayer, synth)
+from paper_2305_13525_b200 import (MOE_F_AUX_LOSS, MOE_F_CAC, MOE_F_CHECKPOINT,  # noqa: E402
+                                   MOE_F_NCCL_EXCHANGE, MOE_F_RANDOM_PRIORITY, MoEConfig, MoELayer, synth)
 from tests.helpers import REL_L2_BAR, bf16_tensor, rel_l2, tensor_f64  # noqa: E402
 
 
@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--ffn", type=int, default=512)
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--cf", type=float, default=1.0)
+    ap.add_argument("--variants", action="store_true",
+                    help="also run top-2 + random priority + aux loss (NEXT #4), DTD and vanilla")
     a = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -163,6 +165,8 @@ def main():
     a2a_van = v["stats"]["wire_bytes"]["a2a"]
     if a2a_dtd * a.gt != a2a_van:
         failures.append(f"a2a bytes: dtd {a2a_dtd} x {a.gt} != vanilla {a2a_van}")
+    if a.variants:
+        failures += check_variants(a, world, rank, dev, shape, xs_b, dys_b, wg, w1_b, w2_b)
     print(f"[rank {rank}] (d,ep,t)=({L['d']},{L['ep']},{L['t']}) errs="
           + " ".join(f"{k}={e:.2e}" for k, e in errs.items())
           + f" a2a dtd={a2a_dtd} van={a2a_van} calls={t_['stats']['calls']}"
@@ -171,6 +175,80 @@ def main():
     dist.all_reduce(flag)
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 0 else 1)
+
+
+def check_variants(a, world, rank, dev, shape, xs_b, dys_b, wg, w1_b, w2_b):
+    """Top-2 (R22) with random priority (R20) and the aux loss (R21) through the exchange:
+    parity with oracle/top2_oracle.py and DTD == vanilla bitwise (G_t <= 2)."""
+    from oracle import top2_oracle as T2
+    failures = []
+    seed, coef = 4242, 0.03
+    res = {}
+    for dtd in (True, False):
+        cfg = MoEConfig.from_shape(shape, dtd=dtd)
+        cfg = MoEConfig(cfg.tokens, cfg.hidden, cfg.ffn, cfg.experts, cfg.capacity_factor, cfg.g_tensor,
+                        cfg.g_expert, cfg.dtd, cfg.flags | MOE_F_RANDOM_PRIORITY | MOE_F_AUX_LOSS, coef, top_k=2)
+        layer = MoELayer(cfg, world, rank, dev)
+        layer.moe_set_priority_seed(seed)
+        L = layer.layout
+        s = L["d"] * a.gep + L["ep"]
+        w1s, w2s = synth.shard_experts(w1_b, w2_b, shape, L["ep"], L["t"])
+        x, dy = bf16_tensor(xs_b[s]), bf16_tensor(dys_b[s])
+        wgt = torch.from_numpy(wg).to(dev)
+        w1t, w2t = bf16_tensor(w1s), bf16_tensor(w2s)
+        y, saved = layer.moe_forward(x, wgt, w1t, w2t)
+        dx, dwg, dw1, dw2 = layer.moe_backward(dy, saved, x, wgt, w1t, w2t)
+        rt = layer.moe_routing(saved)
+        aux = layer.moe_aux_loss(saved)
+        torch.cuda.synchronize()
+        res[dtd] = {"y": y, "dx": dx, "dwg": dwg, "dw1": dw1, "dw2": dw2, "aux": aux.item(),
+                    "rt": {k: v.cpu().numpy() for k, v in rt.items()}, "L": L, "s": s}
+        layer.close()
+    g = res[True]
+    L = g["L"]
+    groups = [L["d"] * a.gep + ep for ep in range(a.gep)]
+    xs = [O.decode_bf16(xs_b[q]) for q in groups]
+    dys = [O.decode_bf16(dys_b[q]) for q in groups]
+    ge = torch.from_numpy(g["rt"]["expert"]).to(dev)
+    gg = torch.from_numpy(g["rt"]["gap"]).to(dev)
+    all_e = [torch.empty_like(ge) for _ in range(world)]
+    all_g = [torch.empty_like(gg) for _ in range(world)]
+    dist.all_gather(all_e, ge)
+    dist.all_gather(all_g, gg)
+    cap = T2.capacity_top2(a.tokens, a.experts, a.cf, a.gt)
+    order = O.priority_order(a.tokens, seed)
+    overrides = []
+    for gi, q in enumerate(groups):
+        ex = all_e[q * a.gt].cpu().numpy()
+        gp = all_g[q * a.gt].cpu().numpy()
+        r0 = T2.route_top2(xs[gi], wg.astype(np.float64), cap, order=order)
+        tie = (r0.gap < O.TIE_GAP) | (gp < O.TIE_GAP)
+        if ((ex != r0.experts).any(axis=1) & ~tie).any():
+            failures.append(f"variants: top-2 routing mismatch outside ties (group {q})")
+        overrides.append((np.nonzero(tie)[0], ex[tie]))
+    ref = T2.layer_top2(xs, dys, wg.astype(np.float64), O.decode_bf16(w1_b), O.decode_bf16(w2_b), a.cf, a.gt,
+                        overrides=overrides, order=order, aux_coef=coef)
+    gi = groups.index(g["s"])
+    r = ref["routing"][gi]
+    if not (g["rt"]["slot"] == r.slot).all():
+        failures.append("variants: slot mismatch")
+    El, Fl = L["experts_local"], L["ffn_local"]
+    es = slice(L["ep"] * El, (L["ep"] + 1) * El)
+    fs = slice(L["t"] * Fl, (L["t"] + 1) * Fl)
+    errs = {"y": rel_l2(tensor_f64(g["y"]), ref["y"][gi]), "dx": rel_l2(tensor_f64(g["dx"]), ref["dx"][gi]),
+            "dwg": rel_l2(g["dwg"].cpu().numpy(), ref["dwg"][gi]),
+            "dw1": rel_l2(tensor_f64(g["dw1"]), ref["dw1"][es, fs, :]),
+            "dw2": rel_l2(tensor_f64(g["dw2"]), ref["dw2"][es, :, fs])}
+    for k, v in errs.items():
+        if not v <= REL_L2_BAR:
+            failures.append(f"variants: {k} rel L2 {v:.3e}")
+    if abs(g["aux"] - ref["aux"][gi]) > 1e-5 * abs(ref["aux"][gi]):
+        failures.append(f"variants: aux {g['aux']} vs {ref['aux'][gi]}")
+    for k in ("y", "dx", "dwg", "dw1", "dw2"):
+        if a.gt <= 2 and not torch.equal(res[True][k], res[False][k]):
+            failures.append(f"variants: DTD != vanilla (bitwise) for {k}")
+    print(f"[rank {rank}] variants errs=" + " ".join(f"{k}={e:.2e}" for k, e in errs.items()), flush=True)
+    return failures
 
 
 if __name__ == "__main__":

@@ -53,6 +53,9 @@ def test_status_strings():
     (dict(capacity_factor=0.0), "MOE_ERR_ARG"),
     (dict(flags=256), "MOE_ERR_ARG"),
     (dict(flags=128, aux_loss_coef=-1.0), "MOE_ERR_ARG"),
+    (dict(top_k=3), "MOE_ERR_ARG"),
+    (dict(top_k=2, experts=1), "MOE_ERR_SHAPE"),
+    (dict(top_k=2, flags=2), "MOE_ERR_UNSUPPORTED"),        # forced routing is top-1 only
 ])
 def test_config_validation(kw, status):
     base = dict(tokens=16384, hidden=2048, ffn=8192, experts=16)
@@ -61,6 +64,17 @@ def test_config_validation(kw, status):
     with pytest.raises(MoEError) as ei:
         moe_plan_bytes(cfg, 1, 0)
     assert ei.value.name == status and ei.value.detail
+
+
+def test_top2_capacity_and_saved_bytes():
+    """R22: C = ceil(cf * 2T / E) (rounded to G_t); per-token routing arrays double."""
+    from oracle import top2_oracle as T2
+    for T, E, cf, gt in [(16384, 16, 1.0, 1), (1000, 5, 0.7, 1), (4096, 16, 1.25, 2)]:
+        c2 = MoEConfig(T, 2048, 8192, E, cf, gt, 1, top_k=2)
+        assert moe_plan_layout(c2, gt, 0)["capacity"] == T2.capacity_top2(T, E, cf, gt)
+    one = moe_plan_bytes(MoEConfig(16384, 2048, 8192, 16), 1, 0)[0]
+    two = moe_plan_bytes(MoEConfig(16384, 2048, 8192, 16, top_k=2), 1, 0)[0]
+    assert two > one  # twice the slot space plus the [T][2] routing arrays
 
 
 def test_world_must_factor():

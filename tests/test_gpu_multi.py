@@ -13,13 +13,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CASES = [  # (world, G_t, G_ep, extra args)
-    (2, 1, 2, []),
-    (2, 2, 1, []),
+    (2, 1, 2, ["--variants"]),         # + top-2 / random priority / aux loss (NEXT #4)
+    (2, 2, 1, ["--variants"]),
     (2, 1, 1, []),                     # pure data parallel: no collectives
     (4, 2, 2, []),
     (4, 1, 4, ["--experts", "16"]),
     (4, 4, 1, []),
-    (4, 2, 2, ["--cf", "0.5"]),        # drops under DTD
+    (4, 2, 2, ["--cf", "0.5", "--variants"]),  # drops under DTD
     (8, 2, 4, ["--experts", "16"]),
     (8, 1, 8, ["--experts", "32"]),
     (8, 4, 2, []),
