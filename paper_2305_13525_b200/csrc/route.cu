@@ -31,7 +31,7 @@ __device__ __forceinline__ int wp_index(int e, int hl, int hch) {
 }
 
 __device__ __forceinline__ void stage_wg_pairs(float* ws, const float* __restrict__ wg, int h0,
-                                               int hch, int H, int E, int emax) {
+                                               int hch, int H, int E, int emax, int e0) {
   constexpr int U = 16;
   const int n = hch * emax;
   const int nt = blockDim.x;
@@ -41,7 +41,7 @@ __device__ __forceinline__ void stage_wg_pairs(float* ws, const float* __restric
     for (int k = 0; k < U; ++k) {
       const int i = b + k * nt;
       const int hl = i / emax, e = i - hl * emax;
-      v[k] = (i < n && e < E && h0 + hl < H) ? __ldg(wg + (size_t)(h0 + hl) * E + e) : 0.f;
+      v[k] = (i < n && e0 + e < E && h0 + hl < H) ? __ldg(wg + (size_t)(h0 + hl) * E + e0 + e) : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -52,6 +52,75 @@ __device__ __forceinline__ void stage_wg_pairs(float* ws, const float* __restric
       }
     }
   }
+}
+
+// Routing decision of one token from its E logits (R1, R4, R5; top-2: R22).
+template <int EMAX>
+__device__ __forceinline__ void finalize_token(const float (&lv)[EMAX], int64_t tok, int E, int K,
+                                               const int32_t* __restrict__ forced,
+                                               int32_t* __restrict__ expert, float* __restrict__ prob,
+                                               float* __restrict__ gap, int32_t* __restrict__ ties) {
+  float m = -FLT_MAX, m2 = -FLT_MAX;
+  int best = 0;
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    if (e >= E) break;
+    const float v = lv[e];
+    if (v > m) { m2 = m; m = v; best = e; }
+    else if (v > m2) { m2 = v; }
+  }
+  float den = 0.f;
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) {
+    if (e >= E) break;
+    den += expf(lv[e] - m);
+  }
+  if (K == 2) {  // R22: second = lowest-index max over e != best; gap over the top 3
+    float v2 = -FLT_MAX, v3 = -FLT_MAX;
+    int e2 = best == 0 ? 1 : 0;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      if (e >= E) break;
+      if (e == best) continue;
+      const float v = lv[e];
+      if (v > v2) { v3 = v2; v2 = v; e2 = e; }
+      else if (v > v3) { v3 = v; }
+    }
+    const float g = E > 2 ? fminf(m - v2, v2 - v3) : m - v2;
+    const float s1 = 1.f / den, s2 = expf(v2 - m) / den;
+    expert[2 * tok] = best;
+    expert[2 * tok + 1] = e2;
+    prob[2 * tok] = s1 / (s1 + s2);
+    prob[2 * tok + 1] = s2 / (s1 + s2);
+    gap[tok] = g;
+    if (g < 1e-6f) atomicAdd(ties, 1);
+    return;
+  }
+  const int chosen = forced ? forced[tok] : best;
+  float lc = m;
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e)
+    if (e == chosen) lc = lv[e];
+  const float g = (E > 1) ? (m - m2) : FLT_MAX;
+  expert[tok] = chosen;
+  prob[tok] = expf(lc - m) / den;
+  gap[tok] = g;
+  if (g < 1e-6f) atomicAdd(ties, 1);
+}
+
+// Expert-split gate, second pass: one thread per token reads its E logits (written by
+// the logits-only passes) and takes the same routing decision.
+template <int EMAX>
+__global__ void __launch_bounds__(256)
+    gate_finalize_kernel(const float* __restrict__ logits, const int32_t* __restrict__ forced, int64_t T,
+                         int E, int K, int32_t* __restrict__ expert, float* __restrict__ prob,
+                         float* __restrict__ gap, int32_t* __restrict__ ties) {
+  const int64_t tok = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tok >= T) return;
+  float lv[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) lv[e] = e < E ? logits[(size_t)tok * E + e] : -FLT_MAX;
+  finalize_token<EMAX>(lv, tok, E, K, forced, expert, prob, gap, ties);
 }
 
 // One warp owns TPW tokens at a time; lane l covers h = 256 i + 8 l + [0, 8).
@@ -65,9 +134,12 @@ template <int EMAX, int TPW, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     gate_kernel(const bf16* __restrict__ x, const float* __restrict__ wg,
                 const int32_t* __restrict__ forced, int64_t T, int H, int E, int hch, int K,
+                bool logits_only,
                 float* __restrict__ logits, int32_t* __restrict__ expert,
                 float* __restrict__ prob, float* __restrict__ gap, int32_t* __restrict__ ties) {
   constexpr int EP = EMAX / 2;
+  // expert-split pass (logits_only): CTA row blockIdx.y covers experts [e0, e0 + EMAX)
+  const int e0 = logits_only ? (int)blockIdx.y * EMAX : 0;
   extern __shared__ __align__(16) float ws[];  // [EP][2*hch] (see wp_index), then x buffers
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // x double buffer of this warp: [2][TPW][256] bf16
@@ -76,7 +148,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const int nchunks = (H + hch - 1) / hch;
   const bool resident = nchunks == 1;
   if (resident) {
-    stage_wg_pairs(ws, wg, 0, hch, H, E, EMAX);
+    stage_wg_pairs(ws, wg, 0, hch, H, E, EMAX, e0);
     __syncthreads();
   }
   const int64_t nbatch = (T + PER_CTA - 1) / PER_CTA;
@@ -92,7 +164,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       const int h0 = c * hch;
       if (!resident) {
         __syncthreads();
-        stage_wg_pairs(ws, wg, h0, hch, H, E, EMAX);
+        stage_wg_pairs(ws, wg, h0, hch, H, E, EMAX, e0);
         __syncthreads();
       }
       const int hlen = H - h0 < hch ? H - h0 : hch;
@@ -161,53 +233,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         lv[2 * ep] = acc[t][ep].x;
         lv[2 * ep + 1] = acc[t][ep].y;
       }
-      float m = -FLT_MAX, m2 = -FLT_MAX;
-      int best = 0;
+      if (logits_only) {  // expert-split pass: this CTA's EMAX experts starting at e0
 #pragma unroll
-      for (int e = 0; e < EMAX; ++e) {
-        if (e >= E) break;
-        const float v = lv[e];
-        logits[(size_t)tok * E + e] = v;
-        if (v > m) { m2 = m; m = v; best = e; }
-        else if (v > m2) { m2 = v; }
-      }
-      float den = 0.f;
-#pragma unroll
-      for (int e = 0; e < EMAX; ++e) {
-        if (e >= E) break;
-        den += expf(lv[e] - m);
-      }
-      if (K == 2) {  // R22: second = lowest-index max over e != best; gap over the top 3
-        float v2 = -FLT_MAX, v3 = -FLT_MAX;
-        int e2 = best == 0 ? 1 : 0;
-#pragma unroll
-        for (int e = 0; e < EMAX; ++e) {
-          if (e >= E) break;
-          if (e == best) continue;
-          const float v = lv[e];
-          if (v > v2) { v3 = v2; v2 = v; e2 = e; }
-          else if (v > v3) { v3 = v; }
-        }
-        const float g = E > 2 ? fminf(m - v2, v2 - v3) : m - v2;
-        const float s1 = 1.f / den, s2 = expf(v2 - m) / den;
-        expert[2 * tok] = best;
-        expert[2 * tok + 1] = e2;
-        prob[2 * tok] = s1 / (s1 + s2);
-        prob[2 * tok + 1] = s2 / (s1 + s2);
-        gap[tok] = g;
-        if (g < 1e-6f) atomicAdd(ties, 1);
+        for (int e = 0; e < EMAX; ++e)
+          if (e0 + e < E) logits[(size_t)tok * E + e0 + e] = lv[e];
         continue;
       }
-      const int chosen = forced ? forced[tok] : best;
-      float lc = m;
 #pragma unroll
       for (int e = 0; e < EMAX; ++e)
-        if (e == chosen) lc = lv[e];
-      const float g = (E > 1) ? (m - m2) : FLT_MAX;
-      expert[tok] = chosen;
-      prob[tok] = expf(lc - m) / den;
-      gap[tok] = g;
-      if (g < 1e-6f) atomicAdd(ties, 1);
+        if (e < E) logits[(size_t)tok * E + e] = lv[e];
+      finalize_token<EMAX>(lv, tok, E, K, forced, expert, prob, gap, ties);
     }
   }
 }
@@ -428,8 +463,48 @@ cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
   int64_t grid = (a.T + per_cta - 1) / per_cta;
   if (hch >= a.H && grid > g_sms) grid = g_sms;  // Wg resident: persistent over token batches
   gate_kernel<EMAX, TPW, WARPS><<<(unsigned)grid, WARPS * 32, smem, s>>>(
-      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, hch, a.K, a.logits, a.expert,
+      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, hch, a.K, false, a.logits, a.expert,
       a.prob, a.gap, a.ties);
+  return cudaGetLastError();
+}
+
+// Expert split (Wg of all E experts does not fit in 128 KiB of shared memory, e.g.
+// H = 4096 with E = 16, or H = 2560 with E = 32): groups of EG experts whose [H][EG]
+// slice stays resident (<= 160 KiB), one grid row per group, logits only; then
+// gate_finalize_kernel takes the routing decision from the full logit rows.
+constexpr int SPLIT_WG_BYTES = 160 * 1024;
+
+template <int EG>
+cudaError_t launch_gate_split(const RouteArgs& a, int hpad, cudaStream_t s) {
+  constexpr int TPW = 4, WARPS = 16;
+  const int smem = EG * hpad * 4 + WARPS * 2 * TPW * 256 * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gate_kernel<EG, TPW, WARPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SPLIT_WG_BYTES + WARPS * 2 * TPW * 256 * 2);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int groups = (a.E + EG - 1) / EG;
+  const int64_t per_cta = (int64_t)WARPS * TPW;
+  int64_t gx = (a.T + per_cta - 1) / per_cta;
+  const int64_t cap = (g_sms + groups - 1) / groups;
+  if (gx > cap) gx = cap;
+  gate_kernel<EG, TPW, WARPS><<<dim3((unsigned)gx, groups), WARPS * 32, smem, s>>>(
+      static_cast<const bf16*>(a.x), a.wg, a.forced, a.T, a.H, a.E, hpad, a.K, true, a.logits, a.expert,
+      a.prob, a.gap, a.ties);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const unsigned fb = (unsigned)((a.T + 255) / 256);
+  if (a.E <= 16) gate_finalize_kernel<16><<<fb, 256, 0, s>>>(a.logits, a.forced, a.T, a.E, a.K, a.expert, a.prob, a.gap, a.ties);
+  else if (a.E <= 32) gate_finalize_kernel<32><<<fb, 256, 0, s>>>(a.logits, a.forced, a.T, a.E, a.K, a.expert, a.prob, a.gap, a.ties);
+  else gate_finalize_kernel<64><<<fb, 256, 0, s>>>(a.logits, a.forced, a.T, a.E, a.K, a.expert, a.prob, a.gap, a.ties);
   return cudaGetLastError();
 }
 
@@ -444,7 +519,12 @@ cudaError_t route(const RouteArgs& a, cudaStream_t s) {
     if (e == cudaSuccess && a.aux_out) e = cudaMemsetAsync(a.aux_out, 0, sizeof(float) * (a.E + 1), s);
     return e;
   }
-  if (a.E <= 4) e = launch_gate<4, 4, 16>(a, s);
+  const int hpad = (a.H + 255) & ~255;
+  const int emax = a.E <= 4 ? 4 : a.E <= 8 ? 8 : a.E <= 16 ? 16 : a.E <= 32 ? 32 : 64;
+  const bool resident = (int64_t)emax * hpad * 4 <= 128 * 1024;
+  if (!resident && a.E > 4 && (int64_t)16 * hpad * 4 <= SPLIT_WG_BYTES) e = launch_gate_split<16>(a, hpad, s);
+  else if (!resident && a.E > 4 && (int64_t)8 * hpad * 4 <= SPLIT_WG_BYTES) e = launch_gate_split<8>(a, hpad, s);
+  else if (a.E <= 4) e = launch_gate<4, 4, 16>(a, s);
   else if (a.E <= 8) e = launch_gate<8, 4, 16>(a, s);
   else if (a.E <= 16) e = launch_gate<16, 4, 16>(a, s);
   else if (a.E <= 32) e = launch_gate<32, 2, 16>(a, s);

@@ -93,7 +93,9 @@ def test_tiny_forced_routing(mode):
 
 
 @pytest.mark.parametrize("T,H,F,E", [(1000, 128, 192, 5), (2048, 256, 512, 16), (3000, 320, 640, 32),
-                                     (777, 64, 128, 64), (1, 64, 64, 3)])
+                                     (777, 64, 128, 64), (1, 64, 64, 3),
+                                     # expert-split gate (Wg > 128 KiB): 6.7B / 2.7B / E = 64 widths
+                                     (1000, 4096, 256, 16), (600, 2560, 128, 32), (500, 2048, 128, 64)])
 def test_ragged_shapes(T, H, F, E):
     shape = synth.LayerShape("ragged", T, H, F, E)
     inp = Inputs(shape)

@@ -72,7 +72,8 @@ def test_top2_tiny(cf):
 
 
 @pytest.mark.parametrize("T,H,F,E", [(1000, 128, 192, 5), (2048, 256, 512, 16), (3000, 320, 640, 32),
-                                     (777, 64, 128, 64), (64, 64, 64, 2)])
+                                     (777, 64, 128, 64), (64, 64, 64, 2), (700, 4096, 128, 16),
+                                     (500, 2560, 128, 32)])
 def test_top2_ragged(T, H, F, E):
     shape = synth.LayerShape("top2", T, H, F, E)
     inp = Inputs(shape)
