@@ -437,6 +437,40 @@ moe_status exchange_ce(moe_ctx* c, const void* src, int win, int el_lo, int el_h
   return MOE_OK;
 }
 
+// Dispatch-direction pieces of the G_t = 1 split exchange on the copy engines: the
+// staged slot-space rows of every remote rank's experts into that rank's window, at
+// source block `me` ([E_l][G_ep][C][H]).
+moe_status exchange_ce_dispatch(moe_ctx* c, const void* stage, int win, cudaStream_t st) {
+  const Dims& d = c->d;
+  const size_t pb = (size_t)d.C * d.H * 2;
+  for (int ep2 = 0; ep2 < d.Gep; ++ep2) {
+    if (ep2 == d.ep) continue;
+    const int r = d.d * d.Gep + ep2;  // G_t = 1
+    for (int el = 0; el < d.El; ++el) {
+      const uint8_t* src = static_cast<const uint8_t*>(stage) + (size_t)(ep2 * d.El + el) * pb;
+      uint8_t* dst = static_cast<uint8_t*>(c->h_table[(size_t)r * moe_ctx::NWIN + win]) +
+                     ((size_t)el * d.Gep + d.ep) * pb;
+      CUDA_TRY(c, cudaMemcpyAsync(dst, src, pb, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  return MOE_OK;
+}
+
+// Expert GEMM over the rows of source blocks [s0, s1) of every local expert (rows
+// [s0*C, s1*C) of each [G_ep*C]-row batch): strided batches, G_t = 1 split exchange.
+moe_status gemm_rows(moe_ctx* c, GemmArgs g, int s0, int s1, int64_t a_ld, int64_t d_ld, cudaStream_t st) {
+  const Dims& d = c->d;
+  if (s1 <= s0) return MOE_OK;
+  const int64_t r0 = (int64_t)s0 * d.C;
+  g.M = (int)((s1 - s0) * d.C);
+  g.A = static_cast<const uint8_t*>(g.A) + (size_t)r0 * a_ld * 2;
+  g.D = static_cast<uint8_t*>(g.D) + (size_t)r0 * d_ld * 2;
+  if (g.aux) g.aux = static_cast<uint8_t*>(g.aux) + (size_t)r0 * d_ld * 2;
+  g.a_bs = d.R * a_ld;
+  g.d_bs = d.R * d_ld;
+  return gemm(c, g, st);
+}
+
 moe_status exchange_local(moe_ctx* c, const void* src, int win, cudaStream_t st) {
   const Dims& d = c->d;
   CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, c->d_ret_local, c->n_ret_local,
@@ -501,7 +535,22 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   const int32_t* tok_of = at<int32_t>(saved, sv.tok_of);
   const int32_t* count = at<int32_t>(saved, sv.count);
   void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
-  if (d.peer) {
+  // G_t = 1 split exchange: local rows -> own window, remote rows -> stage -> copy engines,
+  // overlapped with GEMM1 on the local source block
+  const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;
+  if (split) {
+    SplitDst sd{X, D, d.ep, d.El, d.Gep};
+    {
+      Scope sc_(c, MOE_K_DISPATCH, st, 1);
+      CUDA_TRY(c, dispatch_split(x, tok_of, count, ss, sd, st));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[3], st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
+    TRY(exchange_ce_dispatch(c, D, moe_ctx::W_X0 + rslot, c->side));
+    TRY(barrier(c, c->side));  // every rank's pieces have landed in every window
+    CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
+    ledger(c, MOE_COLL_A2A, pass, c->disp_bytes[1]);
+  } else if (d.peer) {
     // fused: rows go straight from x into the peers' expert-space windows
     {
       Scope sc_(c, MOE_K_DISPATCH, st, 1);
@@ -520,7 +569,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
       if (d.dtd) TRY(ag_expert(c, pass, X, st));
     }
   }
-  if (d.peer && d.ckpt) {  // CAC stash of the first collective's output
+  if (d.peer && d.ckpt && !split) {  // CAC stash of the first collective's output
     Scope sc_(c, MOE_K_COMM, st, 0);
     CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.X), X, (size_t)d.El * d.R * d.H * 2,
                                 cudaMemcpyDeviceToDevice, st));
@@ -532,7 +581,22 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
   void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
   GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
-  TRY(gemm(c, g1, st));
+  if (split) {
+    TRY(gemm_rows(c, g1, d.ep, d.ep + 1, d.H, d.Fl, st));  // own block: already in place
+    {
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[3], 0));
+    }
+    TRY(gemm_rows(c, g1, 0, d.ep, d.H, d.Fl, st));
+    TRY(gemm_rows(c, g1, d.ep + 1, d.Gep, d.H, d.Fl, st));
+    if (d.ckpt) {  // CAC stash of the first collective's output
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.X), X, (size_t)d.El * d.R * d.H * 2,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    TRY(gemm(c, g1, st));
+  }
   if (d.peer) {
     // F7 GEMM2 in two expert halves; each half's TP reduction and return pieces (F8-F10)
     // go out on the side stream (copy engines) while the next half computes
@@ -826,7 +890,20 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   void* dS = d.peer ? c->win[moe_ctx::W_DS] : at<uint8_t>(c->scratch, sc.dS);
 
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
-  if (d.peer) {
+  const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;  // as in forward_core
+  if (split) {
+    SplitDst sd{dY, dO, d.ep, d.El, d.Gep};
+    {
+      Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
+      CUDA_TRY(c, combine_bwd_split(dy, O, expert, slot, prob, count, ss, d.T, dp, sd, st));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[3], st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
+    TRY(exchange_ce_dispatch(c, dO, moe_ctx::W_DY, c->side));
+    TRY(barrier(c, c->side));
+    CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
+    ledger(c, MOE_COLL_A2A, 1, c->disp_bytes[1]);
+  } else if (d.peer) {
     {
       Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
       CUDA_TRY(c, combine_bwd_peer(dy, O, expert, slot, prob, count, nullptr, ss, d.T, lo, hi, dp,
@@ -847,7 +924,17 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   }
   // B4 dHpre = (dY W2) * G; B5 dXpart = dHpre W1; B6 dW2 = dY^T A, dW1 = dHpre^T X
   GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(G)};
-  TRY(gemm(c, g4, st));
+  if (split) {
+    TRY(gemm_rows(c, g4, d.ep, d.ep + 1, d.H, d.Fl, st));  // own block overlaps the copy engines
+    {
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[3], 0));
+    }
+    TRY(gemm_rows(c, g4, 0, d.ep, d.H, d.Fl, st));
+    TRY(gemm_rows(c, g4, d.ep + 1, d.Gep, d.H, d.Fl, st));
+  } else {
+    TRY(gemm(c, g4, st));
+  }
   GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
   TRY(gemm(c, g5, st));
   GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};

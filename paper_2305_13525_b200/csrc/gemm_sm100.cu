@@ -46,6 +46,7 @@ constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /
 struct Params {
   int batch, M, N, K;
   int tiles_m, tiles_n, total_tiles, k_blocks;
+  int64_t d_bs;  // elements between batches of D / aux
   bf16* D;
   bf16* aux;
 };
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       const int mrow0 = m0 + quad * 32;
       const int m = mrow0 + lane;
       const bool row_ok = m < p.M;
-      const size_t row_off = ((size_t)b * p.M + (row_ok ? m : 0)) * (size_t)p.N;
+      const size_t row_off = (size_t)b * p.d_bs + (size_t)(row_ok ? m : 0) * (size_t)p.N;
 #pragma unroll 1
       for (int c = col0; c < col0 + COLS_W; c += 32) {
         const int n = n0 + c;
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
           const uint32_t off = row * 64 + ((qq ^ ((row >> 1) & 3)) << 4);
           const int mm = mrow0 + row;
           const bool ok = mm < p.M && col_ok;
-          const size_t go = ((size_t)b * p.M + mm) * (size_t)p.N + n + qq * 8;
+          const size_t go = (size_t)b * p.d_bs + (size_t)mm * (size_t)p.N + n + qq * 8;
           const uint4 vd = ld_shared_v4(bD + off);
           if (ok) st_v4(p.D + go, vd);
           if (EPI == EPI_GELU) {
@@ -532,9 +533,9 @@ void init_once() {
 // 3-D bf16 tensor map {inner, outer, batch}, box {box_inner, box_outer, 1}.
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t batch,
               uint32_t box_inner, uint32_t box_outer,
-              CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
+              CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B, uint64_t batch_stride = 0) {
   cuuint64_t dims[3] = {inner, outer, batch};
-  cuuint64_t strides[2] = {inner * 2, inner * outer * 2};
+  cuuint64_t strides[2] = {inner * 2, (batch_stride ? batch_stride : inner * outer) * 2};
   cuuint32_t box[3] = {box_inner, box_outer, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
@@ -591,14 +592,20 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   if (g_init_err != cudaSuccess) { *why = "driver entry point / device query failed"; return g_init_err; }
   if (a.batch <= 0 || a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaSuccess;
   const bool pair = a.variant != 1;  // default: CTA-pair (cta_group::2) kernel
+  if ((a.a_bs || a.d_bs) && (!pair || a.a_mn)) {
+    *why = "batch strides need the CTA-pair kernel and a K-major A";
+    return cudaErrorNotSupported;
+  }
   CUtensorMap ta, tb;
   bool ok = a.a_mn ? make_map(&ta, a.A, a.M, a.K, a.batch, 64, 64)
-                   : make_map(&ta, a.A, a.K, a.M, a.batch, 64, BM);
+                   : make_map(&ta, a.A, a.K, a.M, a.batch, 64, BM, CU_TENSOR_MAP_SWIZZLE_128B,
+                              (uint64_t)a.a_bs);
   ok = ok && (a.b_mn ? make_map(&tb, a.B, a.N, a.K, a.batch, 64, 64)
                      : make_map(&tb, a.B, a.K, a.N, a.batch, 64, pair ? 128 : BN));
   if (!ok) { *why = "cuTensorMapEncodeTiled rejected the operand layout"; return cudaErrorInvalidValue; }
   Params p;
   p.batch = a.batch; p.M = a.M; p.N = a.N; p.K = a.K;
+  p.d_bs = a.d_bs ? a.d_bs : (int64_t)a.M * a.N;
   p.tiles_m = (a.M + (pair ? 256 : BM) - 1) / (pair ? 256 : BM);
   p.tiles_n = (a.N + BN - 1) / BN;
   p.total_tiles = p.tiles_m * p.tiles_n * a.batch;

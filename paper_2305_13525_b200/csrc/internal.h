@@ -20,6 +20,10 @@ struct GemmArgs {
   int epilogue;
   void* aux;  // EPI_GELU: out A = gelu(acc) [b][M][N] (D = gelu'(acc)); EPI_DGELU: in G [b][M][N] (D = acc*G)
   int variant = 0;  // 0: CTA-pair kernel (cta_group::2, product path); 1: single-CTA kernel
+  // Batch strides in elements (0 = dense): rows [0, M) of batch b of A (K-major only)
+  // start at A + b * a_bs; of D / aux at D + b * d_bs (a row block of a larger batch,
+  // e.g. the rows of one source rank inside [E_l][G_ep][C]). CTA-pair kernel only.
+  int64_t a_bs = 0, d_bs = 0;
 };
 
 // tcgen05 / TMEM / TMA kernel (the product path).
@@ -132,5 +136,19 @@ cudaError_t adamw_fused(const void* grad, float* p, float* m, float* v, void* p1
                         const AdamwScalars& s, cudaStream_t st);
 cudaError_t adamw_tiled(const void* grad, float* p, float* m, float* v, void* p16, int64_t n,
                         const AdamwScalars& s, int64_t ts, float* temp, cudaStream_t st, int* launches);
+
+// (permute.cu) G_t = 1 split exchange: rows of this rank's experts -> its own window
+// (loc, expert space [E_l][G_ep][C][H], source block me), others -> stage (slot space
+// [E][C][H]) for the copy-engine pieces of exchange_ce_dispatch.
+struct SplitDst {
+  void* loc;    // bf16
+  void* stage;  // bf16
+  int me, El, Gep;
+};
+cudaError_t dispatch_split(const void* x, const int32_t* tok_of, const int32_t* count,
+                           const SlotSpace& ss, const SplitDst& sd, cudaStream_t s);
+cudaError_t combine_bwd_split(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
+                              const float* prob, const int32_t* count, const SlotSpace& ss, int64_t T,
+                              float* dp, const SplitDst& sd, cudaStream_t s);
 
 }  // namespace moe

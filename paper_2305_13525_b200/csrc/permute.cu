@@ -323,6 +323,95 @@ __global__ void __launch_bounds__(WARPS * 32)
   __threadfence_system();
 }
 
+// ---------------------------------------------------------------- split variants (G_t = 1)
+// Rows of this rank's own experts go straight into its expert-space window
+// ([E_l][G_ep][C] rows, source block = me); rows of remote experts go to a dense
+// slot-space staging buffer, from which the copy engines move them to the peers
+// (exchange_ce_dispatch) while the expert GEMM runs on the local block.
+__device__ __forceinline__ bf16* split_row(const SplitDst& sd, const SlotSpace& ss, int e, int64_t c) {
+  const int owner = e / sd.El;
+  if (owner == sd.me)
+    return static_cast<bf16*>(sd.loc) + (((size_t)(e - owner * sd.El) * sd.Gep + sd.me) * ss.C + c) * ss.H;
+  return static_cast<bf16*>(sd.stage) + ((size_t)e * ss.C + c) * ss.H;
+}
+
+__global__ void __launch_bounds__(WARPS * 32)
+    dispatch_split_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ tok_of,
+                          const int32_t* __restrict__ count, SlotSpace ss, int64_t rows, SplitDst sd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int e = (int)(r / ss.C);
+  const int64_t c = r % ss.C;
+  bf16* dst = split_row(sd, ss, e, c);
+  const int nv = ss.H / 8;
+  if (c < count[e]) copy_row<false>(x + (size_t)(tok_of[(size_t)e * ss.C + c] / ss.K) * ss.H, dst, nv, lane);
+  else copy_row<true>(nullptr, dst, nv, lane);
+}
+
+__global__ void __launch_bounds__(WARPS * 32)
+    combine_bwd_split_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ O,
+                             const int32_t* __restrict__ expert, const int32_t* __restrict__ slot,
+                             const float* __restrict__ prob, SlotSpace ss, int64_t T,
+                             float* __restrict__ dp, SplitDst sd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (t >= T) return;
+  for (int kc = 0; kc < ss.K; ++kc) {
+    const int64_t it = t * ss.K + kc;
+    const int s = slot[it];
+    if (s < 0) {
+      if (lane == 0) dp[it] = 0.f;
+      continue;
+    }
+    const int e = expert[it];
+    const float p = prob[it];
+    const bf16* dyr = dy + (size_t)t * ss.H;
+    const bf16* orow = O + slot_row(ss, e, s);
+    bf16* dst = split_row(sd, ss, e, s);
+    const int nv = ss.H / 8;
+    float acc = 0.f;
+    constexpr int U = 4;
+    for (int v0 = 0; v0 < nv; v0 += 32 * U) {
+      uint4 a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        a[u] = v < nv ? ld_nc_v4(dyr + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+        b[u] = v < nv ? ld_nc_v4(orow + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        uint32_t wa[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+        uint32_t wb[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float2 fa = unpack_bf16x2(wa[k]), fb = unpack_bf16x2(wb[k]);
+          acc = fmaf(fa.x, fb.x, acc);
+          acc = fmaf(fa.y, fb.y, acc);
+          w[k] = pack_bf16x2(p * fa.x, p * fa.y);
+        }
+        if (v < nv) st_v4(dst + (size_t)v * 8, make_uint4(w[0], w[1], w[2], w[3]));
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) dp[it] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(WARPS * 32)
+    zero_empty_split_kernel(const int32_t* __restrict__ count, SlotSpace ss, int64_t rows, SplitDst sd) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int e = (int)(r / ss.C);
+  const int64_t c = r % ss.C;
+  if (c < count[e]) return;
+  copy_row<true>(nullptr, split_row(sd, ss, e, c), ss.H / 8, lane);
+}
+
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + WARPS - 1) / WARPS); }
 
 }  // namespace
@@ -382,6 +471,26 @@ cudaError_t combine_bwd_peer(const void* dy, const void* O, const int32_t* exper
   const int64_t rows = (int64_t)(t_hi - t_lo) * ss.E * ss.Cs;
   if (rows > 0)
     zero_empty_peer_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(count, ss, t_lo, rows, pd);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_split(const void* x, const int32_t* tok_of, const int32_t* count,
+                           const SlotSpace& ss, const SplitDst& sd, cudaStream_t s) {
+  const int64_t rows = (int64_t)ss.E * ss.C;
+  if (rows <= 0) return cudaSuccess;
+  dispatch_split_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(static_cast<const bf16*>(x), tok_of, count,
+                                                                 ss, rows, sd);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_bwd_split(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
+                              const float* prob, const int32_t* count, const SlotSpace& ss, int64_t T,
+                              float* dp, const SplitDst& sd, cudaStream_t s) {
+  if (T > 0)
+    combine_bwd_split_kernel<<<blocks_for(T), WARPS * 32, 0, s>>>(
+        static_cast<const bf16*>(dy), static_cast<const bf16*>(O), expert, slot, prob, ss, T, dp, sd);
+  const int64_t rows = (int64_t)ss.E * ss.C;
+  if (rows > 0) zero_empty_split_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(count, ss, rows, sd);
   return cudaGetLastError();
 }
 

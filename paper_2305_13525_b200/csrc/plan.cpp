@@ -122,7 +122,10 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->local_rank = f.take((size_t)d.T * d.K * 4);
   sc->block_hist = f.take((size_t)((d.T * d.K + 1023) / 1024) * d.E * 4);
   sc->auxp = d.aux ? f.take((size_t)AUX_GRID * d.E * 8) : 0;  // P partials + first-choice counts
-  sc->D = (solo || d.peer) ? 0 : f.take(slot_space);  // peer mode dispatches straight into windows
+  // peer mode dispatches straight into windows; with G_t = 1 (split exchange) the rows of
+  // remote experts are staged in slot space for the copy engines
+  const bool split = d.peer && d.Gt == 1 && d.Gep > 1;
+  sc->D = solo ? 0 : (d.peer ? (split ? f.take(slot_space) : 0) : f.take(slot_space));
   sc->Ypart = solo ? 0 : f.take(expert_space);
   Bump b;  // backward region reuses the forward region
   sc->dp = b.take((size_t)d.T * d.K * 4);
@@ -130,7 +133,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));
   sc->dY = d.peer ? 0 : b.take(expert_space);   // peer mode: window WdY
-  sc->dO = solo ? sc->dY : (d.peer ? 0 : b.take(slot_space));
+  sc->dO = solo ? sc->dY : (d.peer ? (split ? b.take(slot_space) : 0) : b.take(slot_space));
   sc->dH = b.take(ffn_space);
   sc->dXp = b.take(expert_space);
   sc->dS = solo ? sc->dXp : (d.peer ? 0 : b.take(slot_space));  // peer mode: window WdS
