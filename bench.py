@@ -458,21 +458,26 @@ def main():
                "collectives": {"calls": st["calls"], "wire_bytes": st["wire_bytes"]},
                "optimizer": optim}
         if world > 1:
-            # a2a bandwidth: bytes this rank sends to other ranks per step over the
-            # time of the kernel classes that move them. In peer mode (default) the dispatch and
-            # combine-backward kernels store straight into the peers' windows and the return
-            # exchanges run in the comm class; their local HBM work is included in the time, so
-            # the figure is a lower bound on the link rate.
+            # a2a bandwidth: bytes this rank sends to other ranks per step. In peer
+            # mode every remote piece of a G_t = 1 layer travels on the copy engines (class "xfer",
+            # CUDA events on the side stream around the copies, overlapped with the GEMMs), so
+            # egress / xfer time is the link rate achieved; otherwise (fused SM stores / NCCL) the
+            # time basis is the kernel classes that move the bytes, a lower bound.
             wb = {k: v / args.steps for k, v in st["wire_bytes"].items()}
             egress = sum(wb.values())
-            ex_ms = per_class["comm"] + per_class["dispatch"] + per_class["combine_bwd"]
+            xfer_ms = per_class.get("xfer", 0.0)
+            if xfer_ms > 0 and gt == 1:
+                ex_ms, basis = xfer_ms, "copy-engine transfers (xfer class, side stream)"
+            else:
+                ex_ms = per_class["comm"] + per_class["dispatch"] + per_class["combine_bwd"] + xfer_ms
+                basis = "comm + dispatch + combine_bwd + xfer classes (lower bound)"
             gbs = egress / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None
             out["comm_ms_per_step"] = per_class["comm"]
             out["a2a"] = {"a2a_bytes_per_step": wb["a2a"], "egress_bytes_per_step": egress,
-                          "exchange_ms_per_step": ex_ms, "egress_GB/s": gbs,
+                          "transfer_ms_per_step": ex_ms, "egress_GB/s": gbs,
                           "peak_GB/s": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                          "frac": gbs / 770.0 if gbs else None,
-                          "time_basis": "comm + dispatch + combine_bwd kernel classes (CUDA events)"}
+                          "frac": gbs / 770.0 if gbs else None, "time_basis": basis,
+                          "exposed_comm_ms_per_step": per_class["comm"]}
         print(json.dumps(out), flush=True)
     layer.close()
     if dist is not None:

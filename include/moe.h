@@ -148,7 +148,9 @@ enum { MOE_K_ROUTE = 0,       /* F1 gate + F2 slot scan                 */
        MOE_K_COMBINE_BWD = 4, /* B1                                     */
        MOE_K_GATE_BWD = 5,    /* B10                                    */
        MOE_K_COMM = 6,        /* NCCL collectives + self-chunk copies   */
-       MOE_K_CLASSES = 7 };
+       MOE_K_XFER = 7,        /* copy-engine exchange transfers (side stream, overlapped;
+                                 timed, no kernels)                      */
+       MOE_K_CLASSES = 8 };
 
 typedef struct {
   int64_t calls[MOE_COLL_KINDS];

@@ -24,7 +24,7 @@ MOE_F_CHECKPOINT = 16
 MOE_F_CAC = 32
 MOE_F_RANDOM_PRIORITY = 64
 MOE_F_AUX_LOSS = 128
-KERNEL_CLASSES = ("route", "dispatch", "gemm", "combine", "combine_bwd", "gate_bwd", "comm")
+KERNEL_CLASSES = ("route", "dispatch", "gemm", "combine", "combine_bwd", "gate_bwd", "comm", "xfer")
 COLL_NAMES = ("a2a", "allgather", "reducescatter", "allreduce")
 
 
@@ -62,7 +62,7 @@ class _Stats(ctypes.Structure):
                 ("forward_calls", ctypes.c_int64), ("backward_calls", ctypes.c_int64),
                 ("dropped_tokens", ctypes.c_int64), ("tie_tokens", ctypes.c_int64),
                 ("nccl_async_error", ctypes.c_int32),
-                ("kernel_launches", ctypes.c_int64 * 7), ("kernel_ms", ctypes.c_double * 7),
+                ("kernel_launches", ctypes.c_int64 * 8), ("kernel_ms", ctypes.c_double * 8),
                 ("replay_calls", ctypes.c_int64)]
 
 
