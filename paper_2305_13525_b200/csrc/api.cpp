@@ -546,7 +546,10 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[3], st));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
-    TRY(exchange_ce_dispatch(c, D, moe_ctx::W_X0 + rslot, c->side));
+    {
+      Scope sx_(c, MOE_K_XFER, c->side, 0);
+      TRY(exchange_ce_dispatch(c, D, moe_ctx::W_X0 + rslot, c->side));
+    }
     TRY(barrier(c, c->side));  // every rank's pieces have landed in every window
     CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
     ledger(c, MOE_COLL_A2A, pass, c->disp_bytes[1]);
@@ -616,7 +619,10 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
         if (d.dtd) TRY(rs_expert(c, pass, Y, c->side, e0, e1, e0 == 0));
         else TRY(ar_expert(c, pass, Y, c->side, e0, e1, e0 == 0));
       }
-      TRY(exchange_ce(c, Y, moe_ctx::W_O0 + rslot, e0, e1, c->side));
+      {
+        Scope sx_(c, MOE_K_XFER, c->side, 0);
+        TRY(exchange_ce(c, Y, moe_ctx::W_O0 + rslot, e0, e1, c->side));
+      }
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[2], c->side));
     Scope sc_(c, MOE_K_COMM, st, 0);
@@ -899,7 +905,10 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[3], st));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
-    TRY(exchange_ce_dispatch(c, dO, moe_ctx::W_DY, c->side));
+    {
+      Scope sx_(c, MOE_K_XFER, c->side, 0);
+      TRY(exchange_ce_dispatch(c, dO, moe_ctx::W_DY, c->side));
+    }
     TRY(barrier(c, c->side));
     CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
     ledger(c, MOE_COLL_A2A, 1, c->disp_bytes[1]);
@@ -954,7 +963,10 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       if (d.dtd) TRY(rs_expert(c, 1, dXp, c->side));
       else TRY(ar_expert(c, 1, dXp, c->side));
     }
-    TRY(exchange_ce(c, dXp, moe_ctx::W_DS, 0, d.El, c->side));
+    {
+      Scope sx_(c, MOE_K_XFER, c->side, 0);
+      TRY(exchange_ce(c, dXp, moe_ctx::W_DS, 0, d.El, c->side));
+    }
     CUDA_TRY(c, cudaEventRecord(c->ev[1], c->side));
     if (c->overlap) {
       TRY(gemm(c, g6, st));
