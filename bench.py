@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=None, choices=[None, "1.3b", "2.7b", "6.7b"])
     p.add_argument("--vanilla", action="store_true", help="disable DTD (G_tensor > 1 configs)")
+    p.add_argument("--gt", type=int, default=None, help="G_tensor override (BASELINE scaling sweep)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-optim", action="store_true", help="skip the tiled-optimizer measurement")
@@ -88,12 +89,24 @@ def measure_optimizer(dw1, dw2, peaks, steps, dev):
 def workload(args, world):
     """(name, tokens/group, H, F, E, G_t, G_ep)."""
     cfg = args.config or "1.3b"
-    if cfg == "1.3b":
-        return ("1.3b-ep%d" % world if world > 1 else "1.3b", 16384, 2048, 8192, 16, 1, world)
-    if cfg == "2.7b":
-        return ("2.7b-ep%d" % world, 16384, 2560, 10240, 32, 1, world)
-    gt = 2 if world >= 2 else 1
-    return ("6.7b-tp%dep%d" % (gt, world // gt), 16384, 4096, 16384, 16, gt, world // gt)
+    shapes = {"1.3b": (2048, 8192, 16), "2.7b": (2560, 10240, 32), "6.7b": (4096, 16384, 16)}
+    H, F, E = shapes[cfg]
+    if args.gt:
+        gt = args.gt
+    elif cfg == "6.7b":
+        gt = 2 if world >= 2 else 1
+    else:
+        gt = 1
+    if world % gt:
+        raise SystemExit(f"--gt {gt} does not divide {world} GPUs")
+    gep = world // gt
+    if cfg == "1.3b" and world == 1:
+        name = "1.3b"
+    elif gt == 1:
+        name = f"{cfg}-ep{gep}"
+    else:
+        name = f"{cfg}-tp{gt}ep{gep}"
+    return (name, 16384, H, F, E, gt, gep)
 
 
 def load_peaks():
