@@ -13,7 +13,8 @@ def main(path, kern, n=40):
                           "-k", f"regex:{kern}"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+    data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr) and r != hdr]
+    data = [d for d in data if (d["Warp Stall Sampling (All Samples)"] or "0").isdigit()]
     tot = sum(int(d["Warp Stall Sampling (All Samples)"] or 0) for d in data)
     print(f"{len(data)} SASS lines, {tot} stall samples")
     # window view: print hot lines in address order with their samples
