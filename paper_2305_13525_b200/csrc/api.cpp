@@ -41,7 +41,9 @@ struct moe_ctx {
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
-  enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, W_FLAGS = 6, NWIN = 7 };
+  // W_Y / W_DXP: the TP partials of GEMM2 / B5, read by the TP partners (G_t > 1)
+  enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, W_FLAGS = 6, W_Y = 7, W_DXP = 8,
+         NWIN = 9 };
   uint32_t epoch = 0;  // flag-barrier epoch
   void* win[NWIN] = {};
   std::vector<void*> opened;
@@ -327,8 +329,10 @@ moe_status setup_peer(moe_ctx* c) {
   const Dims& d = c->d;
   const size_t expert_space = (size_t)d.El * d.R * d.H * 2;
   const size_t slot_space = (size_t)d.E * d.C * d.H * 2;
+  const size_t tp_space = d.Gt > 1 ? expert_space : 256;
   const size_t sizes[moe_ctx::NWIN] = {expert_space, expert_space, slot_space, slot_space,
-                                       expert_space, slot_space, (size_t)256 * ((d.world + 63) / 64)};
+                                       expert_space, slot_space, (size_t)256 * ((d.world + 63) / 64),
+                                       tp_space, tp_space};
   std::vector<cudaIpcMemHandle_t> mine(moe_ctx::NWIN);
   for (int w = 0; w < moe_ctx::NWIN; ++w) {
     CUDA_TRY(c, cudaMalloc(&c->win[w], sizes[w]));
@@ -471,6 +475,10 @@ moe_status gemm_rows(moe_ctx* c, GemmArgs g, int s0, int s1, int64_t a_ld, int64
   return gemm(c, g, st);
 }
 
+// G_t > 1: barrier (every TP partial complete), fused TP reduction + return exchange,
+// barrier (every destination written). Same ledger as the NCCL-mode RS/AR + a2a (+AG).
+moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_t st);
+
 moe_status exchange_local(moe_ctx* c, const void* src, int win, cudaStream_t st) {
   const Dims& d = c->d;
   CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, c->d_ret_local, c->n_ret_local,
@@ -483,6 +491,28 @@ moe_status barrier(moe_ctx* c, cudaStream_t st) {
   const Dims& d = c->d;
   CUDA_TRY(c, peer_barrier(c->d_table, moe_ctx::NWIN, moe_ctx::W_FLAGS, d.world, d.rank, ++c->epoch, st));
   c->stats.kernel_launches[MOE_K_COMM] += 1;
+  return MOE_OK;
+}
+
+moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_t st) {
+  const Dims& d = c->d;
+  TRY0(barrier(c, st));
+  ReduceReturn rr;
+  rr.table = c->d_table;
+  rr.nwin = moe_ctx::NWIN;
+  rr.src_win = src_win;
+  rr.dst_win = dst_win;
+  rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E; rr.H = d.H;
+  rr.Cs = d.Cs;
+  rr.dtd = d.dtd ? 1 : 0;
+  CUDA_TRY(c, reduce_return(rr, st));
+  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  TRY0(barrier(c, st));
+  const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
+  if (d.dtd) ledger(c, MOE_COLL_REDUCESCATTER, pass, xe * (d.Gt - 1) / d.Gt);
+  else ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * xe * (d.Gt - 1) / d.Gt);
+  if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
+  if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
   return MOE_OK;
 }
 
@@ -582,7 +612,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   void* G = d.ckpt ? at<uint8_t>(c->scratch, sc.Grec) : at<uint8_t>(saved, sv.G);
   void* A = d.ckpt ? at<uint8_t>(c->scratch, sc.Arec) : at<uint8_t>(saved, sv.A);
   void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
-  void* Y = sc.Y_in_saved ? O : at<uint8_t>(c->scratch, sc.Ypart);
+  void* Y = sc.Y_in_saved ? O : (d.peer && d.Gt > 1 ? c->win[moe_ctx::W_Y] : at<uint8_t>(c->scratch, sc.Ypart));
   GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
   if (split) {
     TRY(gemm_rows(c, g1, d.ep, d.ep + 1, d.H, d.Fl, st));  // own block: already in place
@@ -600,10 +630,21 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   } else {
     TRY(gemm(c, g1, st));
   }
-  if (d.peer) {
+  if (d.peer && d.Gt > 1) {
+    // F7 GEMM2 into the TP-visible window, then F8-F10 as one fused kernel over peer
+    // memory (NCCL's reduce-scatter would wait for the persistent GEMMs to free SMs)
+    GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+    TRY(gemm(c, g2, st));
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(tp_return(c, pass, moe_ctx::W_Y, moe_ctx::W_O0 + rslot, st));
+    if (d.ckpt) {  // CAC stash of the second collective's output
+      CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.O), O, (size_t)d.E * d.C * d.H * 2,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+  } else if (d.peer) {
     // F7 GEMM2 in two expert halves; each half's TP reduction and return pieces (F8-F10)
     // go out on the side stream (copy engines) while the next half computes
-    const int h = c->overlap && d.El >= 2 && d.Gt == 1 ? d.El / 2 : d.El;
+    const int h = c->overlap && d.El >= 2 ? d.El / 2 : d.El;
     const size_t rows = (size_t)d.R * d.H;
     for (int part = 0; part < 2; ++part) {
       const int e0 = part == 0 ? 0 : h, e1 = part == 0 ? h : d.El;
@@ -892,7 +933,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   void* dY = d.peer ? c->win[moe_ctx::W_DY] : at<uint8_t>(c->scratch, sc.dY);
   void* dO = at<uint8_t>(c->scratch, sc.dO);
   void* dH = at<uint8_t>(c->scratch, sc.dH);
-  void* dXp = at<uint8_t>(c->scratch, sc.dXp);
+  void* dXp = d.peer && d.Gt > 1 ? c->win[moe_ctx::W_DXP] : at<uint8_t>(c->scratch, sc.dXp);
   void* dS = d.peer ? c->win[moe_ctx::W_DS] : at<uint8_t>(c->scratch, sc.dS);
 
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
@@ -948,7 +989,31 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   TRY(gemm(c, g5, st));
   GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};
   GemmArgs g7{d.El, d.Fl, d.H, (int)d.R, dH, 1, X, 1, dw1, EPI_STORE, nullptr};
-  if (d.peer) {
+  if (d.peer && d.Gt > 1) {
+    // B7-B9 fused over peer memory (tp_return), then the weight-gradient GEMMs
+    {
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      TRY(barrier(c, st));  // every TP partial of dX complete
+      ReduceReturn rr;
+      rr.table = c->d_table;
+      rr.nwin = moe_ctx::NWIN;
+      rr.src_win = moe_ctx::W_DXP;
+      rr.dst_win = moe_ctx::W_DS;
+      rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E;
+      rr.H = d.H; rr.Cs = d.Cs; rr.dtd = d.dtd ? 1 : 0;
+      CUDA_TRY(c, reduce_return(rr, st));
+      c->stats.kernel_launches[MOE_K_COMM] += 1;
+    }
+    TRY(gemm(c, g6, st));
+    TRY(gemm(c, g7, st));
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(barrier(c, st));  // every destination written (each rank's reduce precedes its barrier)
+    const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
+    if (d.dtd) ledger(c, MOE_COLL_REDUCESCATTER, 1, xe * (d.Gt - 1) / d.Gt);
+    else ledger(c, MOE_COLL_ALLREDUCE, 1, 2 * xe * (d.Gt - 1) / d.Gt);
+    if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
+    if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
+  } else if (d.peer) {
     // B7-B9 (TP reduction + return pieces) on the side stream, overlapping the
     // weight-gradient GEMMs, which do not feed them
     CUDA_TRY(c, cudaEventRecord(c->ev[0], st));

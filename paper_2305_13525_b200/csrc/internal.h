@@ -104,6 +104,17 @@ struct Piece {
 };
 cudaError_t peer_exchange(const void* src, void* const* d_table, int nwin, int win,
                           const Piece* d_pieces, int npieces, size_t piece_bytes, cudaStream_t s);
+// (peer.cu) fused TP reduction + return exchange for G_t > 1: reads the TP partials of
+// window src_win (expert space) on every TP rank of this rank's group, writes the sums
+// into window dst_win (slot space) of the source ranks.
+struct ReduceReturn {
+  void* const* table;  // device [world][nwin]
+  int nwin, src_win, dst_win;
+  int d, ep, t, Gt, Gep, El, E, H;
+  int64_t Cs;
+  int dtd;
+};
+cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s);
 // Flag barrier over the peer windows (window `win` holds one uint32 slot per rank).
 cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
                          uint32_t epoch, cudaStream_t s);

@@ -58,7 +58,86 @@ __global__ void peer_barrier_kernel(void* const* __restrict__ table, int nwin, i
   } while ((int32_t)(v - epoch) < 0);
 }
 
+// Fused TP reduction + return exchange (F8-F10 / B7-B9 for G_t > 1): one warp per
+// expert-space row of the slices this rank reduces (DTD: its own slot slice t; vanilla:
+// all slices), summing the G_t partials of the TP group in fixed order t' = 0..G_t-1 in
+// fp32 (partners' windows read over NVLink), rounding once to bf16 and storing the row
+// into the slot-space window of the source rank(s): every TP rank of the source under
+// DTD (the folded all-gather), the same-t rank under vanilla. With G_t = 2 this equals
+// NCCL's bf16 sum bit for bit.
+constexpr int RR_WARPS = 8;
+__global__ void __launch_bounds__(RR_WARPS * 32)
+    reduce_return_kernel(ReduceReturn rr, int64_t rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * RR_WARPS + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int nsl = rr.dtd ? 1 : rr.Gt;  // slices reduced by this rank
+  const int64_t cs = r % rr.Cs;
+  int64_t q = r / rr.Cs;
+  const int src = (int)(q % rr.Gep);
+  q /= rr.Gep;
+  const int tt = rr.dtd ? rr.t : (int)(q % nsl);
+  const int el = (int)(q / nsl);
+  const size_t rowb = (size_t)rr.H * 2;
+  const size_t xoff = ((((size_t)el * rr.Gt + tt) * rr.Gep + src) * rr.Cs + cs) * rowb;
+  const int e = rr.ep * rr.El + el;
+  const size_t ooff = (((size_t)tt * rr.E + e) * rr.Cs + cs) * rowb;
+  const int nv = rr.H / 8;
+  const int tp0 = (rr.d * rr.Gep + rr.ep) * rr.Gt;
+  const int dst0 = (rr.d * rr.Gep + src) * rr.Gt;
+  constexpr int U = 4;
+  for (int v0 = 0; v0 < nv; v0 += 32 * U) {
+    float acc[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[u][k] = 0.f;
+    for (int tp = 0; tp < rr.Gt; ++tp) {
+      const uint8_t* base = static_cast<const uint8_t*>(rr.table[(size_t)(tp0 + tp) * rr.nwin + rr.src_win]) + xoff;
+      uint4 b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        b[u] = v < nv ? ld_nc_v4(base + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t w[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = unpack_bf16x2(w[k]);
+          acc[u][2 * k] += f.x;
+          acc[u][2 * k + 1] += f.y;
+        }
+      }
+    }
+    uint4 o[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      o[u] = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
+                        pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
+    const int nd = rr.dtd ? rr.Gt : 1;
+    for (int k = 0; k < nd; ++k) {
+      const int dr = dst0 + (rr.dtd ? k : rr.t);
+      uint8_t* dst = static_cast<uint8_t*>(rr.table[(size_t)dr * rr.nwin + rr.dst_win]) + ooff;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nv) st_v4(dst + (size_t)v * 16, o[u]);
+      }
+    }
+  }
+  __threadfence_system();
+}
+
 }  // namespace
+
+cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s) {
+  const int64_t rows = (int64_t)rr.El * rr.Gep * rr.Cs * (rr.dtd ? 1 : rr.Gt);
+  if (rows <= 0) return cudaSuccess;
+  reduce_return_kernel<<<(unsigned)((rows + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, 0, s>>>(rr, rows);
+  return cudaGetLastError();
+}
 
 cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
                          uint32_t epoch, cudaStream_t s) {

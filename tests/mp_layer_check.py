@@ -144,11 +144,15 @@ def main():
             failures.append(f"DTD != vanilla (bitwise) for {k}")
         if not same and rel_l2(tensor_f64(v[k]), tensor_f64(t_[k])) > 1e-2:
             failures.append(f"DTD vs vanilla differ for {k}")
-    # ---- peer-memory exchange vs NCCL exchange (same arithmetic, same positions)
+    # ---- peer-memory exchange vs NCCL exchange (same arithmetic, same positions; the TP
+    # sum of G_t > 2 partials is fixed-order fp32 in the peer kernel and NCCL's ring order in
+    # NCCL mode, so bitwise only for G_t <= 2, where a + b is order-free)
     nc = results["nccl"]
     for k in ("y", "dx", "dwg", "dw1", "dw2"):
-        if not torch.equal(nc[k], t_[k]):
+        if a.gt <= 2 and not torch.equal(nc[k], t_[k]):
             failures.append(f"peer exchange != NCCL exchange (bitwise) for {k}")
+        if rel_l2(tensor_f64(nc[k]), tensor_f64(t_[k])) > 1e-2:
+            failures.append(f"peer exchange vs NCCL exchange differ for {k}")
     if nc["stats"]["wire_bytes"] != t_["stats"]["wire_bytes"]:
         failures.append(f"ledger differs: peer {t_['stats']['wire_bytes']} nccl {nc['stats']['wire_bytes']}")
     # ---- checkpointing: replay (with / without CAC) reproduces the run bitwise; CAC's replay
