@@ -59,6 +59,7 @@ struct moe_ctx {
   cudaStream_t side = nullptr;     // copy-engine / overlap stream
   bool overlap = true;             // MOE_NO_OVERLAP=1: serial return exchanges (A/B knob)
   cudaEvent_t ev[4] = {};
+  cudaEvent_t evp[4] = {};  // GEMM2 parts (G_t = 1 return overlap)
   int64_t disp_bytes[3] = {0, 0, 0}, ret_bytes[3] = {0, 0, 0};  // by Piece::kind
   float* d_barrier = nullptr;
   uint64_t gen = 0;
@@ -378,6 +379,7 @@ moe_status setup_peer(moe_ctx* c) {
   CUDA_TRY(c, cudaMemcpy(c->d_ret_local, loc.data(), sizeof(Piece) * loc.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+  for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
   c->n_disp = (int)disp.size();
   c->n_ret = (int)ret.size();
   CUDA_TRY(c, cudaMalloc(&c->d_disp, sizeof(Piece) * (disp.size() + 1)));
@@ -392,8 +394,10 @@ moe_status setup_peer(moe_ctx* c) {
 
 void teardown_peer(moe_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->evp[i]) cudaEventDestroy(c->evp[i]);
+  }
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   c->opened.clear();
   for (int w = 0; w < moe_ctx::NWIN; ++w)
@@ -642,24 +646,21 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
                                   cudaMemcpyDeviceToDevice, st));
     }
   } else if (d.peer) {
-    // F7 GEMM2 in two expert halves; each half's TP reduction and return pieces (F8-F10)
-    // go out on the side stream (copy engines) while the next half computes
-    const int h = c->overlap && d.El >= 2 ? d.El / 2 : d.El;
+    // (G_t = 1) F7 GEMM2 in up to 4 expert parts; each part's return pieces (F9) go out on
+    // the side stream (copy engines) while the next part computes, so only the last part's
+    // pieces are exposed
+    const int P = c->overlap ? (d.El < 4 ? d.El : 4) : 1;
     const size_t rows = (size_t)d.R * d.H;
-    for (int part = 0; part < 2; ++part) {
-      const int e0 = part == 0 ? 0 : h, e1 = part == 0 ? h : d.El;
+    for (int part = 0; part < P; ++part) {
+      const int e0 = part * d.El / P, e1 = (part + 1) * d.El / P;
       if (e1 <= e0) continue;
       const size_t ao = (size_t)e0 * d.R * d.Fl * 2, yo = (size_t)e0 * rows * 2;
       GemmArgs g2{e1 - e0, (int)d.R, d.H, d.Fl, at<uint8_t>(A, ao), 0,
                   at<uint8_t>(const_cast<void*>(w2), (size_t)e0 * d.H * d.Fl * 2), 0,
                   at<uint8_t>(Y, yo), EPI_STORE, nullptr};
       TRY(gemm(c, g2, st));
-      CUDA_TRY(c, cudaEventRecord(c->ev[part], st));
-      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[part], 0));
-      if (d.Gt > 1) {
-        if (d.dtd) TRY(rs_expert(c, pass, Y, c->side, e0, e1, e0 == 0));
-        else TRY(ar_expert(c, pass, Y, c->side, e0, e1, e0 == 0));
-      }
+      CUDA_TRY(c, cudaEventRecord(c->evp[part], st));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->evp[part], 0));
       {
         Scope sx_(c, MOE_K_XFER, c->side, 0);
         TRY(exchange_ce(c, Y, moe_ctx::W_O0 + rslot, e0, e1, c->side));
