@@ -44,6 +44,9 @@ struct moe_ctx {
   // W_Y / W_DXP: the TP partials of GEMM2 / B5, read by the TP partners (G_t > 1)
   enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, W_FLAGS = 6, W_Y = 7, W_DXP = 8,
          NWIN = 9 };
+  // W_FLAGS: barrier slots [0, world), per-source readiness slots from SIG_OFF
+  enum { SIG_OFF = 4096 };
+  uint32_t sig_epoch = 0;
   uint32_t epoch = 0;  // flag-barrier epoch
   void* win[NWIN] = {};
   std::vector<void*> opened;
@@ -332,7 +335,7 @@ moe_status setup_peer(moe_ctx* c) {
   const size_t slot_space = (size_t)d.E * d.C * d.H * 2;
   const size_t tp_space = d.Gt > 1 ? expert_space : 256;
   const size_t sizes[moe_ctx::NWIN] = {expert_space, expert_space, slot_space, slot_space,
-                                       expert_space, slot_space, (size_t)256 * ((d.world + 63) / 64),
+                                       expert_space, slot_space, (size_t)moe_ctx::SIG_OFF + 4 * (size_t)d.world,
                                        tp_space, tp_space};
   std::vector<cudaIpcMemHandle_t> mine(moe_ctx::NWIN);
   for (int w = 0; w < moe_ctx::NWIN; ++w) {
@@ -445,14 +448,19 @@ moe_status exchange_ce(moe_ctx* c, const void* src, int win, int el_lo, int el_h
   return MOE_OK;
 }
 
-// Dispatch-direction pieces of the G_t = 1 split exchange on the copy engines: the
-// staged slot-space rows of every remote rank's experts into that rank's window, at
-// source block `me` ([E_l][G_ep][C][H]).
-moe_status exchange_ce_dispatch(moe_ctx* c, const void* stage, int win, cudaStream_t st) {
+// Dispatch-direction pieces of the G_t = 1 split exchange on the copy engines: the staged
+// slot-space rows of every remote rank's experts go into that rank's window at source
+// block `me` ([E_l][G_ep][C][H]).
+// Per-source pipelined variant: the pieces for each destination (staggered order
+// me+1, me+2, ... so that every rank receives from one source at a time) followed by a
+// readiness flag in that destination's flag region; returns the epoch to wait for.
+moe_status exchange_ce_dispatch_sig(moe_ctx* c, const void* stage, int win, cudaStream_t st, uint32_t* epoch) {
   const Dims& d = c->d;
   const size_t pb = (size_t)d.C * d.H * 2;
-  for (int ep2 = 0; ep2 < d.Gep; ++ep2) {
-    if (ep2 == d.ep) continue;
+  const uint32_t ep = ++c->sig_epoch;
+  *epoch = ep;
+  for (int k = 1; k < d.Gep; ++k) {
+    const int ep2 = (d.ep + k) % d.Gep;
     const int r = d.d * d.Gep + ep2;  // G_t = 1
     for (int el = 0; el < d.El; ++el) {
       const uint8_t* src = static_cast<const uint8_t*>(stage) + (size_t)(ep2 * d.El + el) * pb;
@@ -460,7 +468,20 @@ moe_status exchange_ce_dispatch(moe_ctx* c, const void* stage, int win, cudaStre
                      ((size_t)el * d.Gep + d.ep) * pb;
       CUDA_TRY(c, cudaMemcpyAsync(dst, src, pb, cudaMemcpyDeviceToDevice, st));
     }
+    uint32_t* flag = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(
+        c->h_table[(size_t)r * moe_ctx::NWIN + moe_ctx::W_FLAGS]) + moe_ctx::SIG_OFF) + d.ep;
+    CUDA_TRY(c, peer_signal(flag, ep, st));
+    c->stats.kernel_launches[MOE_K_COMM] += 1;
   }
+  return MOE_OK;
+}
+
+// Waits (on st) until source block `src`'s pieces of exchange `epoch` are in this rank's window.
+moe_status wait_source(moe_ctx* c, int src, uint32_t epoch, cudaStream_t st) {
+  const uint32_t* flag = reinterpret_cast<const uint32_t*>(
+      static_cast<uint8_t*>(c->win[moe_ctx::W_FLAGS]) + moe_ctx::SIG_OFF) + src;
+  CUDA_TRY(c, peer_wait(flag, epoch, st));
+  c->stats.kernel_launches[MOE_K_COMM] += 1;
   return MOE_OK;
 }
 
@@ -572,6 +593,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   // G_t = 1 split exchange: local rows -> own window, remote rows -> stage -> copy engines,
   // overlapped with GEMM1 on the local source block
   const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;
+  uint32_t sig = 0;
   if (split) {
     SplitDst sd{X, D, d.ep, d.El, d.Gep};
     {
@@ -582,10 +604,8 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
     {
       Scope sx_(c, MOE_K_XFER, c->side, 0);
-      TRY(exchange_ce_dispatch(c, D, moe_ctx::W_X0 + rslot, c->side));
+      TRY(exchange_ce_dispatch_sig(c, D, moe_ctx::W_X0 + rslot, c->side, &sig));
     }
-    TRY(barrier(c, c->side));  // every rank's pieces have landed in every window
-    CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
     ledger(c, MOE_COLL_A2A, pass, c->disp_bytes[1]);
   } else if (d.peer) {
     // fused: rows go straight from x into the peers' expert-space windows
@@ -619,13 +639,17 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   void* Y = sc.Y_in_saved ? O : (d.peer && d.Gt > 1 ? c->win[moe_ctx::W_Y] : at<uint8_t>(c->scratch, sc.Ypart));
   GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
   if (split) {
-    TRY(gemm_rows(c, g1, d.ep, d.ep + 1, d.H, d.Fl, st));  // own block: already in place
-    {
-      Scope sc_(c, MOE_K_COMM, st, 0);
-      CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[3], 0));
+    // own block first (already in place), then each source block as its pieces land
+    // (source me-k sends to me as its k-th destination)
+    TRY(gemm_rows(c, g1, d.ep, d.ep + 1, d.H, d.Fl, st));
+    for (int k = 1; k < d.Gep; ++k) {
+      const int src = (d.ep - k + d.Gep) % d.Gep;
+      {
+        Scope sc_(c, MOE_K_COMM, st, 0);
+        TRY(wait_source(c, src, sig, st));
+      }
+      TRY(gemm_rows(c, g1, src, src + 1, d.H, d.Fl, st));
     }
-    TRY(gemm_rows(c, g1, 0, d.ep, d.H, d.Fl, st));
-    TRY(gemm_rows(c, g1, d.ep + 1, d.Gep, d.H, d.Fl, st));
     if (d.ckpt) {  // CAC stash of the first collective's output
       Scope sc_(c, MOE_K_COMM, st, 0);
       CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.X), X, (size_t)d.El * d.R * d.H * 2,
@@ -939,6 +963,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
 
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
   const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;  // as in forward_core
+  uint32_t sig = 0;
   if (split) {
     SplitDst sd{dY, dO, d.ep, d.El, d.Gep};
     {
@@ -949,10 +974,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
     {
       Scope sx_(c, MOE_K_XFER, c->side, 0);
-      TRY(exchange_ce_dispatch(c, dO, moe_ctx::W_DY, c->side));
+      TRY(exchange_ce_dispatch_sig(c, dO, moe_ctx::W_DY, c->side, &sig));
     }
-    TRY(barrier(c, c->side));
-    CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
     ledger(c, MOE_COLL_A2A, 1, c->disp_bytes[1]);
   } else if (d.peer) {
     {
@@ -977,12 +1000,14 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(G)};
   if (split) {
     TRY(gemm_rows(c, g4, d.ep, d.ep + 1, d.H, d.Fl, st));  // own block overlaps the copy engines
-    {
-      Scope sc_(c, MOE_K_COMM, st, 0);
-      CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[3], 0));
+    for (int k = 1; k < d.Gep; ++k) {
+      const int src = (d.ep - k + d.Gep) % d.Gep;
+      {
+        Scope sc_(c, MOE_K_COMM, st, 0);
+        TRY(wait_source(c, src, sig, st));
+      }
+      TRY(gemm_rows(c, g4, src, src + 1, d.H, d.Fl, st));
     }
-    TRY(gemm_rows(c, g4, 0, d.ep, d.H, d.Fl, st));
-    TRY(gemm_rows(c, g4, d.ep + 1, d.Gep, d.H, d.Fl, st));
   } else {
     TRY(gemm(c, g4, st));
   }

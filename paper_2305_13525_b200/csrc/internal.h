@@ -115,6 +115,10 @@ struct ReduceReturn {
   int dtd;
 };
 cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s);
+// (peer.cu) one-sided readiness flag: store `epoch` to flag (a peer's flag slot) after the
+// stream's prior work; wait until *flag >= epoch (wrap-safe).
+cudaError_t peer_signal(uint32_t* flag, uint32_t epoch, cudaStream_t s);
+cudaError_t peer_wait(const uint32_t* flag, uint32_t epoch, cudaStream_t s);
 // Flag barrier over the peer windows (window `win` holds one uint32 slot per rank).
 cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
                          uint32_t epoch, cudaStream_t s);

@@ -130,7 +130,33 @@ __global__ void __launch_bounds__(RR_WARPS * 32)
   __threadfence_system();
 }
 
+// Point-to-point readiness flags (per-source pipelining of the split exchange): the
+// source stores `epoch` (release, system scope) into slot `src` of the destination's
+// flag region after its copies to that destination; the destination's stream spins
+// (acquire) on that slot before the GEMM over that source's rows.
+__global__ void peer_signal_kernel(uint32_t* flag, uint32_t epoch) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
+__global__ void peer_wait_kernel(const uint32_t* flag, uint32_t epoch) {
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  } while ((int32_t)(v - epoch) < 0);
+}
+
 }  // namespace
+
+cudaError_t peer_signal(uint32_t* flag, uint32_t epoch, cudaStream_t s) {
+  peer_signal_kernel<<<1, 1, 0, s>>>(flag, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t peer_wait(const uint32_t* flag, uint32_t epoch, cudaStream_t s) {
+  peer_wait_kernel<<<1, 1, 0, s>>>(flag, epoch);
+  return cudaGetLastError();
+}
 
 cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s) {
   const int64_t rows = (int64_t)rr.El * rr.Gep * rr.Cs * (rr.dtd ? 1 : rr.Gt);
