@@ -38,6 +38,7 @@ struct moe_ctx {
   ncclComm_t world_comm = nullptr, tp_comm = nullptr, ep_comm = nullptr;
   bool poisoned = false;
   uint64_t priority_seed = 0;  // MOE_F_RANDOM_PRIORITY key (moe_set_priority_seed)
+  bool no_fused_dx = false;    // MOE_NO_FUSED_DX=1: B10 as a separate kernel (A/B, tests)
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
@@ -802,6 +803,10 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
   moe_status s = make_dims(cfg, world, rank, &d, &why);
   if (s != MOE_OK) return fail(s, why);
   moe_ctx* c = new moe_ctx();
+  {
+    const char* nf = std::getenv("MOE_NO_FUSED_DX");
+    c->no_fused_dx = nf && nf[0] == '1';
+  }
   c->d = d;
   c->cfg = *cfg;
   c->timing = (cfg->flags & MOE_F_TIMING) != 0;
@@ -1012,7 +1017,23 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     TRY(gemm(c, g4, st));
   }
   GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
+  // One GPU, top-1, no aux loss: B5's epilogue adds B10's gate term and writes dx rows
+  // directly (no dXp round trip, no separate dx gather); dl is computed before B5.
+  const bool fused_dx = solo && d.K == 1 && !d.aux && d.E % 4 == 0 && d.E <= 32 && !c->no_fused_dx;
+  GateDxArgs gdx{at<int32_t>(saved, sv.tok_of), count, at<float>(c->scratch, sc.dl), wg, d.E, d.C, dx};
+  if (fused_dx) {
+    {
+      Scope sc_(c, MOE_K_GATE_BWD, st, 1);
+      CUDA_TRY(c, gate_dl(logits, expert, slot, prob, dp, d.T, d.E, at<float>(c->scratch, sc.dl), st));
+    }
+    g5.epilogue = EPI_GATEDX;
+    g5.gdx = &gdx;
+  }
   TRY(gemm(c, g5, st));
+  if (fused_dx) {
+    Scope sc_(c, MOE_K_GATE_BWD, st, 1);
+    CUDA_TRY(c, zero_dropped(slot, d.T, d.H, dx, st));
+  }
   GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};
   GemmArgs g7{d.El, d.Fl, d.H, (int)d.R, dH, 1, X, 1, dw1, EPI_STORE, nullptr};
   if (d.peer && d.Gt > 1) {
@@ -1083,8 +1104,12 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       if (d.dtd) TRY(ag_slot(c, 1, dS, st));
     }
   }
-  // B10 dispatch-bwd + gate-bwd
-  {
+  // B10 dispatch-bwd + gate-bwd (fused path: only dWg is left)
+  if (fused_dx) {
+    Scope sc_(c, MOE_K_GATE_BWD, st, 2);
+    CUDA_TRY(c, gate_dwg(x, at<float>(c->scratch, sc.dl), d.T, d.H, d.E, dwg, at<float>(c->scratch, sc.dwgp),
+                         sc.nsplit, st));
+  } else {
     Scope sc_(c, MOE_K_GATE_BWD, st, 4);
     CUDA_TRY(c, gate_bwd(x, dS, wg, logits, expert, slot, prob, dp, ss, d.T, dx, dwg,
                          at<float>(c->scratch, sc.dl), at<float>(c->scratch, sc.dwgp), sc.nsplit,

@@ -401,6 +401,50 @@ __global__ void dwg_reduce2_kernel(const float* __restrict__ partial, int nsplit
   dwg[i] = s;
 }
 
+// ------------------------------------------------------------------ fused-path pieces
+// dl_tj = dp_t p_t (delta_{j e*} - softmax(l_t)_j) for kept tokens, 0 otherwise (top-1)
+__global__ void __launch_bounds__(256)
+    gate_dl_kernel(const float* __restrict__ logits, const int32_t* __restrict__ expert,
+                   const int32_t* __restrict__ slot, const float* __restrict__ prob,
+                   const float* __restrict__ dp, int64_t T, int E, float* __restrict__ dl) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  float* o = dl + (size_t)t * E;
+  if (slot[t] < 0) {
+    for (int j = 0; j < E; ++j) o[j] = 0.f;
+    return;
+  }
+  const float* lg = logits + (size_t)t * E;
+  float m = -3.402823e38f;
+  for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
+  float den = 0.f;
+  for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
+  const float inv = 1.f / den, gsc = dp[t] * prob[t];
+  const int e = expert[t];
+  for (int j = 0; j < E; ++j) o[j] = gsc * ((j == e ? 1.f : 0.f) - expf(lg[j] - m) * inv);
+}
+
+__global__ void __launch_bounds__(256)
+    zero_dropped_kernel(const int32_t* __restrict__ slot, int64_t T, int H, bf16* __restrict__ dx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T || slot[t] >= 0) return;
+  for (int v = lane; v < H / 8; v += 32) st_v4(dx + (size_t)t * H + (size_t)v * 8, make_uint4(0, 0, 0, 0));
+}
+
+template <int EP>
+cudaError_t dwg_only(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,
+                     int nsplit, cudaStream_t s) {
+  constexpr int NT = EP <= 32 ? 4 : 2;
+  constexpr int HB = 8 * NT * 8;
+  const int64_t tps = ((T + nsplit - 1) / nsplit + DW_TT - 1) / DW_TT * DW_TT;
+  dim3 g2((H + HB - 1) / HB, nsplit);
+  dwg_mma_kernel<EP><<<g2, 256, 0, s>>>(static_cast<const bf16*>(x), dl, T, H, E, tps, partial);
+  const int64_t n = (int64_t)H * E;
+  dwg_reduce2_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(partial, nsplit, n, dwg);
+  return cudaGetLastError();
+}
+
 template <int EPK, int EP, int KC>
 cudaError_t run(const void* x, const void* dS, const float* wg, const float* logits,
                 const int32_t* expert, const int32_t* slot, const float* prob, const float* dp,
@@ -476,6 +520,28 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
   if (ss.E <= 32) return RUN(32, 32);
   return RUN(64, 64);
 #undef RUN
+}
+
+cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* slot, const float* prob,
+                    const float* dp, int64_t T, int E, float* dl, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  gate_dl_kernel<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(logits, expert, slot, prob, dp, T, E, dl);
+  return cudaGetLastError();
+}
+
+cudaError_t zero_dropped(const int32_t* slot, int64_t T, int H, void* dx, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  zero_dropped_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(slot, T, H, static_cast<bf16*>(dx));
+  return cudaGetLastError();
+}
+
+cudaError_t gate_dwg(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,
+                     int nsplit, cudaStream_t s) {
+  if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * H * E, s);
+  if (E <= 8) return dwg_only<8>(x, dl, T, H, E, dwg, partial, nsplit, s);
+  if (E <= 16) return dwg_only<16>(x, dl, T, H, E, dwg, partial, nsplit, s);
+  if (E <= 32) return dwg_only<32>(x, dl, T, H, E, dwg, partial, nsplit, s);
+  return dwg_only<64>(x, dl, T, H, E, dwg, partial, nsplit, s);
 }
 
 int gate_bwd_splits(int64_t T) {

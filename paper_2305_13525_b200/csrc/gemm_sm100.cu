@@ -49,6 +49,7 @@ struct Params {
   int64_t d_bs;  // elements between batches of D / aux
   bf16* D;
   bf16* aux;
+  GateDxArgs g;  // EPI_GATEDX
 };
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
@@ -283,6 +284,7 @@ constexpr int EPI_BUF = 32 * 32 * 2;  // one warp's 32 x 32 bf16 chunk, 64B-swiz
 // epilogues use 8 (32 rows x 128 columns) — measured: dGeLU 0.577 -> 0.552 Mcycles.
 __host__ __device__ constexpr int epi_outs(int epi) { return epi == EPI_GELU ? 2 : 1; }
 __host__ __device__ constexpr int epi_warps(int epi) { return epi == EPI_STORE ? 16 : 8; }
+constexpr int GDX_EMAX = 32;  // EPI_GATEDX: dl row of the lane's token in registers
 __host__ __device__ constexpr int threads2(int epi) { return (4 + epi_warps(epi)) * 32; }
 __host__ __device__ constexpr int epi_smem(int epi) { return epi_warps(epi) * epi_outs(epi) * EPI_BUF; }
 __host__ __device__ constexpr int smem2_bytes(int epi) {
@@ -439,6 +441,17 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       const int m = mrow0 + lane;
       const bool row_ok = m < p.M;
       const size_t row_off = (size_t)b * p.d_bs + (size_t)(row_ok ? m : 0) * (size_t)p.N;
+      int tok = -1;                 // EPI_GATEDX: token of this lane's slot row (-1: empty)
+      float dlr[EPI == EPI_GATEDX ? GDX_EMAX : 1];
+      if (EPI == EPI_GATEDX) {
+        tok = (row_ok && m < p.g.count[b]) ? p.g.tok_of[(size_t)b * p.g.C + m] : -1;
+#pragma unroll
+        for (int j = 0; j < GDX_EMAX; j += 4) {
+          float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (tok >= 0 && j < p.g.E) d4 = *reinterpret_cast<const float4*>(p.g.dl + (size_t)tok * p.g.E + j);
+          dlr[j] = d4.x; dlr[j + 1] = d4.y; dlr[j + 2] = d4.z; dlr[j + 3] = d4.w;
+        }
+      }
 #pragma unroll 1
       for (int c = col0; c < col0 + COLS_W; c += 32) {
         const int n = n0 + c;
@@ -469,6 +482,22 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
             const float2 gg = gelu2(f);
             o[w] = pack_bf16x2(gp.x, gp.y);
             g[w] = pack_bf16x2(gg.x, gg.y);
+          } else if (EPI == EPI_GATEDX) {
+            // + sum_j dl[tok][j] Wg[n + 2w (+1)][j] (Wg rows are the same for every lane)
+            float2 gs = f;
+            const float* w0 = p.g.wg + (size_t)(n + 2 * w) * p.g.E;
+#pragma unroll
+            for (int j = 0; j < GDX_EMAX; j += 4) {
+              if (j < p.g.E) {
+                const float4 a = *reinterpret_cast<const float4*>(w0 + j);
+                const float4 c2 = *reinterpret_cast<const float4*>(w0 + p.g.E + j);
+                gs.x = fmaf(dlr[j], a.x, gs.x); gs.x = fmaf(dlr[j + 1], a.y, gs.x);
+                gs.x = fmaf(dlr[j + 2], a.z, gs.x); gs.x = fmaf(dlr[j + 3], a.w, gs.x);
+                gs.y = fmaf(dlr[j], c2.x, gs.y); gs.y = fmaf(dlr[j + 1], c2.y, gs.y);
+                gs.y = fmaf(dlr[j + 2], c2.z, gs.y); gs.y = fmaf(dlr[j + 3], c2.w, gs.y);
+              }
+            }
+            o[w] = pack_bf16x2(gs.x, gs.y);
           } else {
             o[w] = pack_bf16x2(f.x, f.y);
           }
@@ -489,7 +518,13 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
           const bool ok = mm < p.M && col_ok;
           const size_t go = (size_t)b * p.d_bs + (size_t)mm * (size_t)p.N + n + qq * 8;
           const uint4 vd = ld_shared_v4(bD + off);
-          if (ok) st_v4(p.D + go, vd);
+          if (EPI == EPI_GATEDX) {  // scatter to the token's dx row
+            const int trow = __shfl_sync(0xffffffffu, tok, row);
+            if (trow >= 0 && col_ok)
+              st_v4(static_cast<bf16*>(p.g.dx) + (size_t)trow * p.N + n + qq * 8, vd);
+          } else if (ok) {
+            st_v4(p.D + go, vd);
+          }
           if (EPI == EPI_GELU) {
             const uint4 vx = ld_shared_v4(bX + off);
             if (ok) st_v4(p.aux + go, vx);
@@ -613,6 +648,11 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   p.k_blocks = (a.K + BK - 1) / BK;
   p.D = static_cast<bf16*>(a.D);
   p.aux = static_cast<bf16*>(a.aux);
+  p.g = a.gdx ? *a.gdx : GateDxArgs{};
+  if (a.epilogue == EPI_GATEDX && (!a.gdx || !pair || a.gdx->E > GDX_EMAX || a.gdx->E % 4)) {
+    *why = "gate-dx epilogue needs the CTA-pair kernel and E % 4 == 0, E <= 32";
+    return cudaErrorNotSupported;
+  }
   const int key = a.a_mn * 100 + a.b_mn * 10 + a.epilogue;
   if (pair) {
     switch (key) {
@@ -620,6 +660,7 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
       case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, p, s);
       case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, p, s);
       case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, p, s);
+      case 13:  return launch2<0, 1, EPI_GATEDX>(ta, tb, p, s);
       case 110: return launch2<1, 1, EPI_STORE>(ta, tb, p, s);
       default: break;
     }

@@ -8,7 +8,20 @@
 namespace moe {
 
 // Batched GEMM D[b] = epi(A[b] . B[b]^T); layouts as in moe.h (moe_gemm_bf16).
-enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2 };
+enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_GATEDX = 3 };
+
+// EPI_GATEDX (B5 on one GPU, top-1, no aux loss): the epilogue adds the gate term of
+// B10 and writes dx rows directly: dx[tok_of[e][c]] = bf16(acc + sum_j dl[t][j] Wg[n][j])
+// for kept slots c < count[e]; empty slots are skipped (E % 4 == 0, E <= 32).
+struct GateDxArgs {
+  const int32_t* tok_of;  // [E][C]
+  const int32_t* count;   // [E]
+  const float* dl;        // [T][E]
+  const float* wg;        // [H][E]
+  int E;
+  int64_t C;
+  void* dx;               // bf16 [T][H]
+};
 
 struct GemmArgs {
   int batch, M, N, K;
@@ -24,6 +37,7 @@ struct GemmArgs {
   // start at A + b * a_bs; of D / aux at D + b * d_bs (a row block of a larger batch,
   // e.g. the rows of one source rank inside [E_l][G_ep][C]). CTA-pair kernel only.
   int64_t a_bs = 0, d_bs = 0;
+  const GateDxArgs* gdx = nullptr;  // EPI_GATEDX only
 };
 
 // tcgen05 / TMEM / TMA kernel (the product path).
@@ -93,6 +107,13 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
                      const float* aux_f, float aux_coef, cudaStream_t s);
 int gate_bwd_splits(int64_t T);
+// Pieces of B10 for the fused path (EPI_GATEDX): dl [T][E] before B5; zero dx rows of
+// dropped tokens; dWg = x^T dl (deterministic split-K) after.
+cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* slot, const float* prob,
+                    const float* dp, int64_t T, int E, float* dl, cudaStream_t s);
+cudaError_t zero_dropped(const int32_t* slot, int64_t T, int H, void* dx, cudaStream_t s);
+cudaError_t gate_dwg(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,
+                     int nsplit, cudaStream_t s);
 size_t gate_bwd_pack_bytes(int H, int E);
 
 // (peer.cu) one piece of a peer-memory exchange: C_s x H bytes from src + src_off to

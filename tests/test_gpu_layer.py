@@ -212,3 +212,19 @@ def test_checkpoint_replay_bitwise(cac):
         layer.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_fused_gate_dx_matches_separate_kernel(monkeypatch):
+    """B5's gate-dx epilogue (one GPU, top-1) vs the separate B10 kernel (MOE_NO_FUSED_DX=1):
+    y and the expert gradients bitwise, dx / dWg to rounding (the fused path adds the gate
+    term before the bf16 rounding of the B5 accumulator)."""
+    shape = synth.LayerShape("fdx", 4096, 256, 512, 16)
+    inp = Inputs(shape, skew=1.3)
+    monkeypatch.setenv("MOE_NO_FUSED_DX", "0")
+    a, _ = run_gpu(inp, shape)
+    monkeypatch.setenv("MOE_NO_FUSED_DX", "1")
+    b, _ = run_gpu(inp, shape)
+    for k in ("y", "dw1", "dw2", "slot"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert rel_l2(a["dx"], b["dx"]) < 3e-3 and rel_l2(a["dwg"], b["dwg"]) < 1e-5
+    check_parity(inp, a, 1.0)
