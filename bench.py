@@ -222,7 +222,7 @@ def reference_arm(args, world, rank):
     token sample of the same workload, sized so W + K steps take ~2 minutes."""
     if rank != 0:
         return
-    name, T, H, F, E, gt, gep = workload(args, 1)
+    name, T, H, F, E, gt, gep = workload(args, world)  # the arm's config name; per-token math is the same
     probe = 64
     state = oracle_state(H, F, E, probe)
     t64 = cpu_oracle_step(None, probe, state)
