@@ -39,6 +39,7 @@ struct moe_ctx {
   bool poisoned = false;
   uint64_t priority_seed = 0;  // MOE_F_RANDOM_PRIORITY key (moe_set_priority_seed)
   bool no_fused_dx = false;    // MOE_NO_FUSED_DX=1: B10 as a separate kernel (A/B, tests)
+  bool no_fused_combine = false;  // MOE_NO_FUSED_COMBINE=1: F11 as a separate kernel
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
@@ -595,6 +596,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   // overlapped with GEMM1 on the local source block
   const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;
   uint32_t sig = 0;
+  bool fused_combine = false;
   if (split) {
     SplitDst sd{X, D, d.ep, d.El, d.Gep};
     {
@@ -704,6 +706,14 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     }
   } else {
     GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+    // One GPU, top-1: F11 fused into F7's epilogue (O still stored for the backward)
+    fused_combine = solo && d.K == 1 && y && !c->no_fused_combine;
+    GateDxArgs cmb{at<int32_t>(saved, sv.tok_of), at<int32_t>(saved, sv.count), nullptr, nullptr, d.E, d.C, y,
+                   at<float>(saved, sv.prob)};
+    if (fused_combine) {
+      g2.epilogue = EPI_COMBINE;
+      g2.gdx = &cmb;
+    }
     TRY(gemm(c, g2, st));
     // F8 TP reduce, F9 a2a back, F10 all-gather
     if (!solo) {
@@ -718,7 +728,10 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   }
 
   // F11 combine (not in a checkpoint replay: the layer output is not needed again)
-  if (y) {
+  if (fused_combine) {
+    Scope sc_(c, MOE_K_COMBINE, st, 1);
+    CUDA_TRY(c, zero_dropped(at<int32_t>(saved, sv.slot), d.T, d.H, y, st));
+  } else if (y) {
     Scope sc_(c, MOE_K_COMBINE, st, 1);
     CUDA_TRY(c, combine(O, at<int32_t>(saved, sv.expert), at<int32_t>(saved, sv.slot),
                         at<float>(saved, sv.prob), ss, d.T, y, st));
@@ -806,6 +819,8 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
   {
     const char* nf = std::getenv("MOE_NO_FUSED_DX");
     c->no_fused_dx = nf && nf[0] == '1';
+    const char* nc = std::getenv("MOE_NO_FUSED_COMBINE");
+    c->no_fused_combine = nc && nc[0] == '1';
   }
   c->d = d;
   c->cfg = *cfg;

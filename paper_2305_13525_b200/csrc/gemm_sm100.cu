@@ -282,7 +282,7 @@ constexpr int EPI_BUF = 32 * 32 * 2;  // one warp's 32 x 32 bf16 chunk, 64B-swiz
 // epilogue uses 16 (each warp drains 32 rows x 64 columns per tile); the GeLU
 // (two outputs, ~160 registers) and dGeLU (a lane-per-row read of G per chunk)
 // epilogues use 8 (32 rows x 128 columns) — measured: dGeLU 0.577 -> 0.552 Mcycles.
-__host__ __device__ constexpr int epi_outs(int epi) { return epi == EPI_GELU ? 2 : 1; }
+__host__ __device__ constexpr int epi_outs(int epi) { return (epi == EPI_GELU || epi == EPI_COMBINE) ? 2 : 1; }
 __host__ __device__ constexpr int epi_warps(int epi) { return epi == EPI_STORE ? 16 : 8; }
 constexpr int GDX_EMAX = 32;  // EPI_GATEDX: dl row of the lane's token in registers
 __host__ __device__ constexpr int threads2(int epi) { return (4 + epi_warps(epi)) * 32; }
@@ -290,7 +290,8 @@ __host__ __device__ constexpr int epi_smem(int epi) { return epi_warps(epi) * ep
 __host__ __device__ constexpr int smem2_bytes(int epi) {
   return STAGES2 * (A2_STAGE + B2_STAGE) + epi_smem(epi) + 1024 + 256;
 }
-static_assert(smem2_bytes(EPI_STORE) <= 227 * 1024 && smem2_bytes(EPI_GELU) <= 227 * 1024, "smem");
+static_assert(smem2_bytes(EPI_STORE) <= 227 * 1024 && smem2_bytes(EPI_GELU) <= 227 * 1024 &&
+              smem2_bytes(EPI_COMBINE) <= 227 * 1024, "smem");
 
 __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
@@ -441,8 +442,13 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       const int m = mrow0 + lane;
       const bool row_ok = m < p.M;
       const size_t row_off = (size_t)b * p.d_bs + (size_t)(row_ok ? m : 0) * (size_t)p.N;
-      int tok = -1;                 // EPI_GATEDX: token of this lane's slot row (-1: empty)
+      int tok = -1;                 // EPI_GATEDX / EPI_COMBINE: token of this lane's slot row (-1: empty)
       float dlr[EPI == EPI_GATEDX ? GDX_EMAX : 1];
+      float pscale = 0.f;           // EPI_COMBINE: p_t of that token
+      if (EPI == EPI_COMBINE) {
+        tok = (row_ok && m < p.g.count[b]) ? p.g.tok_of[(size_t)b * p.g.C + m] : -1;
+        pscale = tok >= 0 ? p.g.prob[tok] : 0.f;
+      }
       if (EPI == EPI_GATEDX) {
         tok = (row_ok && m < p.g.count[b]) ? p.g.tok_of[(size_t)b * p.g.C + m] : -1;
 #pragma unroll
@@ -482,6 +488,9 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
             const float2 gg = gelu2(f);
             o[w] = pack_bf16x2(gp.x, gp.y);
             g[w] = pack_bf16x2(gg.x, gg.y);
+          } else if (EPI == EPI_COMBINE) {
+            o[w] = pack_bf16x2(f.x, f.y);                    // O (slot space, for the backward)
+            g[w] = pack_bf16x2(pscale * f.x, pscale * f.y);  // y row of the token
           } else if (EPI == EPI_GATEDX) {
             // + sum_j dl[tok][j] Wg[n + 2w (+1)][j] (Wg rows are the same for every lane)
             float2 gs = f;
@@ -506,7 +515,8 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
         for (int q = 0; q < 4; ++q) {
           const uint32_t off = lane * 64 + ((q ^ swz) << 4);
           st_shared_v4(bD + off, o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-          if (EPI == EPI_GELU) st_shared_v4(bX + off, g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+          if (EPI == EPI_GELU || EPI == EPI_COMBINE)
+            st_shared_v4(bX + off, g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
         }
         __syncwarp();
         const bool col_ok = n + qq * 8 < p.N;
@@ -528,6 +538,11 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
           if (EPI == EPI_GELU) {
             const uint4 vx = ld_shared_v4(bX + off);
             if (ok) st_v4(p.aux + go, vx);
+          }
+          if (EPI == EPI_COMBINE) {  // scatter the weighted row to y
+            const uint4 vx = ld_shared_v4(bX + off);
+            const int trow = __shfl_sync(0xffffffffu, tok, row);
+            if (trow >= 0 && col_ok) st_v4(static_cast<bf16*>(p.g.dx) + (size_t)trow * p.N + n + qq * 8, vx);
           }
         }
         __syncwarp();  // the buffer is rewritten by the next chunk
@@ -649,6 +664,10 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   p.D = static_cast<bf16*>(a.D);
   p.aux = static_cast<bf16*>(a.aux);
   p.g = a.gdx ? *a.gdx : GateDxArgs{};
+  if (a.epilogue == EPI_COMBINE && (!a.gdx || !pair)) {
+    *why = "combine epilogue needs the CTA-pair kernel";
+    return cudaErrorNotSupported;
+  }
   if (a.epilogue == EPI_GATEDX && (!a.gdx || !pair || a.gdx->E > GDX_EMAX || a.gdx->E % 4)) {
     *why = "gate-dx epilogue needs the CTA-pair kernel and E % 4 == 0, E <= 32";
     return cudaErrorNotSupported;
@@ -658,6 +677,7 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
     switch (key) {
       case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, p, s);
       case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, p, s);
+      case 4:   return launch2<0, 0, EPI_COMBINE>(ta, tb, p, s);
       case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, p, s);
       case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, p, s);
       case 13:  return launch2<0, 1, EPI_GATEDX>(ta, tb, p, s);

@@ -8,7 +8,7 @@
 namespace moe {
 
 // Batched GEMM D[b] = epi(A[b] . B[b]^T); layouts as in moe.h (moe_gemm_bf16).
-enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_GATEDX = 3 };
+enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_GATEDX = 3, EPI_COMBINE = 4 };
 
 // EPI_GATEDX (B5 on one GPU, top-1, no aux loss): the epilogue adds the gate term of
 // B10 and writes dx rows directly: dx[tok_of[e][c]] = bf16(acc + sum_j dl[t][j] Wg[n][j])
@@ -20,8 +20,12 @@ struct GateDxArgs {
   const float* wg;        // [H][E]
   int E;
   int64_t C;
-  void* dx;               // bf16 [T][H]
+  void* dx;               // bf16 [T][H] (EPI_COMBINE: y)
+  const float* prob;      // EPI_COMBINE: [T] combine weights
 };
+// EPI_COMBINE (F7 on one GPU, top-1): the epilogue stores O as usual and also
+// y[tok_of[e][c]] = bf16(p_t * acc) for kept slots (F11 fused; uses tok_of, count, C,
+// prob and dx = y of GateDxArgs).
 
 struct GemmArgs {
   int batch, M, N, K;

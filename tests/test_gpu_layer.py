@@ -228,3 +228,19 @@ def test_fused_gate_dx_matches_separate_kernel(monkeypatch):
         np.testing.assert_array_equal(a[k], b[k])
     assert rel_l2(a["dx"], b["dx"]) < 3e-3 and rel_l2(a["dwg"], b["dwg"]) < 1e-5
     check_parity(inp, a, 1.0)
+
+
+def test_fused_combine_matches_separate_kernel(monkeypatch):
+    """F7's combine epilogue (one GPU, top-1) vs the separate F11 kernel
+    (MOE_NO_FUSED_COMBINE=1): every gradient bitwise (O is stored the same way), y to
+    rounding (the fused path scales the fp32 accumulator before the bf16 rounding)."""
+    shape = synth.LayerShape("fcb", 4096, 256, 512, 16)
+    inp = Inputs(shape, skew=1.3)
+    monkeypatch.setenv("MOE_NO_FUSED_COMBINE", "0")
+    a, _ = run_gpu(inp, shape)
+    monkeypatch.setenv("MOE_NO_FUSED_COMBINE", "1")
+    b, _ = run_gpu(inp, shape)
+    for k in ("dx", "dwg", "dw1", "dw2", "slot"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert rel_l2(a["y"], b["y"]) < 3e-3
+    check_parity(inp, a, 1.0)
