@@ -709,7 +709,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     // One GPU, top-1: F11 fused into F7's epilogue (O still stored for the backward)
     fused_combine = solo && d.K == 1 && y && !c->no_fused_combine;
     GateDxArgs cmb{at<int32_t>(saved, sv.tok_of), at<int32_t>(saved, sv.count), nullptr, nullptr, d.E, d.C, y,
-                   at<float>(saved, sv.prob)};
+                   at<float>(saved, sv.prob), nullptr, nullptr};
     if (fused_combine) {
       g2.epilogue = EPI_COMBINE;
       g2.gdx = &cmb;
@@ -1034,14 +1034,17 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
   // One GPU, top-1, no aux loss: B5's epilogue adds B10's gate term and writes dx rows
   // directly (no dXp round trip, no separate dx gather); dl is computed before B5.
-  const bool fused_dx = solo && d.K == 1 && !d.aux && d.E % 4 == 0 && d.E <= 32 && !c->no_fused_dx;
-  GateDxArgs gdx{at<int32_t>(saved, sv.tok_of), count, at<float>(c->scratch, sc.dl), wg, d.E, d.C, dx};
+  const bool fused_dx = solo && d.K == 1 && !d.aux && d.E <= 16 && !c->no_fused_dx;
+  GateDxArgs gdx{at<int32_t>(saved, sv.tok_of), count, at<float>(c->scratch, sc.dl), wg, d.E, d.C, dx,
+                 nullptr, at<uint8_t>(c->scratch, sc.aext), at<uint8_t>(c->scratch, sc.bext)};
   if (fused_dx) {
     {
-      Scope sc_(c, MOE_K_GATE_BWD, st, 1);
+      Scope sc_(c, MOE_K_GATE_BWD, st, 3);
       CUDA_TRY(c, gate_dl(logits, expert, slot, prob, dp, d.T, d.E, at<float>(c->scratch, sc.dl), st));
+      CUDA_TRY(c, gate_ext(at<float>(c->scratch, sc.dl), at<int32_t>(saved, sv.tok_of), count, wg, d.E, d.C,
+                           d.H, at<uint8_t>(c->scratch, sc.aext), at<uint8_t>(c->scratch, sc.bext), st));
     }
-    g5.epilogue = EPI_GATEDX;
+    g5.epilogue = EPI_SCATTER;
     g5.gdx = &gdx;
   }
   TRY(gemm(c, g5, st));

@@ -424,6 +424,41 @@ __global__ void __launch_bounds__(256)
   for (int j = 0; j < E; ++j) o[j] = gsc * ((j == e ? 1.f : 0.f) - expf(lg[j] - m) * inv);
 }
 
+// K-extension operands of EPI_SCATTER (split-bf16 products: hi*hi + lo*hi + hi*lo)
+__global__ void __launch_bounds__(256)
+    gate_ext_a_kernel(const float* __restrict__ dl, const int32_t* __restrict__ tok_of,
+                      const int32_t* __restrict__ count, int E, int64_t C, int64_t rows, bf16* __restrict__ a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (slot row, expert j) pair
+  if (i >= rows * 16) return;
+  const int64_t r = i >> 4;
+  const int j = (int)(i & 15);
+  const int e = (int)(r / C);
+  const int64_t c = r - (int64_t)e * C;
+  float v = 0.f;
+  if (c < count[e] && j < E) v = dl[(size_t)tok_of[r] * E + j];
+  bf16 hi, lo;
+  split_bf16(v, hi, lo);
+  bf16* row = a + (size_t)r * 64;
+  row[j] = hi;
+  row[16 + j] = lo;
+  row[32 + j] = hi;
+  row[48 + j] = __float2bfloat16_rn(0.f);
+}
+
+__global__ void __launch_bounds__(256)
+    gate_ext_b_kernel(const float* __restrict__ wg, int E, int H, bf16* __restrict__ b) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (j, h) pair
+  if (i >= (int64_t)16 * H) return;
+  const int j = (int)(i / H), h = (int)(i - (int64_t)j * H);
+  const float v = j < E ? wg[(size_t)h * E + j] : 0.f;
+  bf16 hi, lo;
+  split_bf16(v, hi, lo);
+  b[(size_t)j * H + h] = hi;
+  b[(size_t)(16 + j) * H + h] = hi;
+  b[(size_t)(32 + j) * H + h] = lo;
+  b[(size_t)(48 + j) * H + h] = __float2bfloat16_rn(0.f);
+}
+
 __global__ void __launch_bounds__(256)
     zero_dropped_kernel(const int32_t* __restrict__ slot, int64_t T, int H, bf16* __restrict__ dx) {
   const int lane = threadIdx.x & 31;
@@ -526,6 +561,15 @@ cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* s
                     const float* dp, int64_t T, int E, float* dl, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   gate_dl_kernel<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(logits, expert, slot, prob, dp, T, E, dl);
+  return cudaGetLastError();
+}
+
+cudaError_t gate_ext(const float* dl, const int32_t* tok_of, const int32_t* count, const float* wg, int E,
+                     int64_t C, int H, void* a_ext, void* b_ext, cudaStream_t s) {
+  const int64_t rows = (int64_t)E * C;
+  gate_ext_a_kernel<<<(unsigned)((rows * 16 + 255) / 256), 256, 0, s>>>(dl, tok_of, count, E, C, rows,
+                                                                         static_cast<bf16*>(a_ext));
+  gate_ext_b_kernel<<<(unsigned)(((int64_t)16 * H + 255) / 256), 256, 0, s>>>(wg, E, H, static_cast<bf16*>(b_ext));
   return cudaGetLastError();
 }
 

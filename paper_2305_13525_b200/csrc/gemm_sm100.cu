@@ -47,9 +47,10 @@ struct Params {
   int batch, M, N, K;
   int tiles_m, tiles_n, total_tiles, k_blocks;
   int64_t d_bs;  // elements between batches of D / aux
+  int k_main;    // EPI_SCATTER: k-blocks of the main operands (the last one is the extension)
   bf16* D;
   bf16* aux;
-  GateDxArgs g;  // EPI_GATEDX
+  GateDxArgs g;  // EPI_SCATTER / EPI_COMBINE
 };
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
@@ -283,8 +284,8 @@ constexpr int EPI_BUF = 32 * 32 * 2;  // one warp's 32 x 32 bf16 chunk, 64B-swiz
 // (two outputs, ~160 registers) and dGeLU (a lane-per-row read of G per chunk)
 // epilogues use 8 (32 rows x 128 columns) — measured: dGeLU 0.577 -> 0.552 Mcycles.
 __host__ __device__ constexpr int epi_outs(int epi) { return (epi == EPI_GELU || epi == EPI_COMBINE) ? 2 : 1; }
-__host__ __device__ constexpr int epi_warps(int epi) { return epi == EPI_STORE ? 16 : 8; }
-constexpr int GDX_EMAX = 32;  // EPI_GATEDX: dl row of the lane's token in registers
+__host__ __device__ constexpr int epi_warps(int epi) { return (epi == EPI_STORE || epi == EPI_SCATTER) ? 16 : 8; }
+constexpr int GDX_EMAX = 16;  // EPI_SCATTER: experts covered by the 64-wide K extension (3 x 16 + pad)
 __host__ __device__ constexpr int threads2(int epi) { return (4 + epi_warps(epi)) * 32; }
 __host__ __device__ constexpr int epi_smem(int epi) { return epi_warps(epi) * epi_outs(epi) * EPI_BUF; }
 __host__ __device__ constexpr int smem2_bytes(int epi) {
@@ -301,6 +302,7 @@ __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
 template <int A_MN, int B_MN, int EPI>
 __global__ void __launch_bounds__(threads2(EPI), 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                  const Params p) {
   constexpr int EW = epi_warps(EPI);
   constexpr int NO = epi_outs(EPI);
@@ -365,17 +367,25 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
           const uint32_t a_dst = smem_u32(smA + stage * A2_STAGE);
           const uint32_t b_dst = smem_u32(smB + stage * B2_STAGE);
           const int k0 = kb * BK;
-          if (A_MN) {
-            tma_load_3d_2sm(a_dst, &tmA, full, m0, k0, b);
-            tma_load_3d_2sm(a_dst + 8192, &tmA, full, m0 + 64, k0, b);
+          if (EPI == EPI_SCATTER && kb >= p.k_main) {
+            // K extension (B10's gate term): A2 = [E][M][64] bf16 K-major, B2 = [64][N]
+            // bf16 MN-major, shared by every batch
+            tma_load_3d_2sm(a_dst, &tmA2, full, 0, m0, b);
+            tma_load_3d_2sm(b_dst, &tmB2, full, n0, 0, 0);
+            tma_load_3d_2sm(b_dst + 8192, &tmB2, full, n0 + 64, 0, 0);
           } else {
-            tma_load_3d_2sm(a_dst, &tmA, full, k0, m0, b);
-          }
-          if (B_MN) {
-            tma_load_3d_2sm(b_dst, &tmB, full, n0, k0, b);
-            tma_load_3d_2sm(b_dst + 8192, &tmB, full, n0 + 64, k0, b);
-          } else {
-            tma_load_3d_2sm(b_dst, &tmB, full, k0, n0, b);
+            if (A_MN) {
+              tma_load_3d_2sm(a_dst, &tmA, full, m0, k0, b);
+              tma_load_3d_2sm(a_dst + 8192, &tmA, full, m0 + 64, k0, b);
+            } else {
+              tma_load_3d_2sm(a_dst, &tmA, full, k0, m0, b);
+            }
+            if (B_MN) {
+              tma_load_3d_2sm(b_dst, &tmB, full, n0, k0, b);
+              tma_load_3d_2sm(b_dst + 8192, &tmB, full, n0 + 64, k0, b);
+            } else {
+              tma_load_3d_2sm(b_dst, &tmB, full, k0, n0, b);
+            }
           }
           if (++stage == STAGES2) { stage = 0; phase ^= 1; }
         }
@@ -442,22 +452,14 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       const int m = mrow0 + lane;
       const bool row_ok = m < p.M;
       const size_t row_off = (size_t)b * p.d_bs + (size_t)(row_ok ? m : 0) * (size_t)p.N;
-      int tok = -1;                 // EPI_GATEDX / EPI_COMBINE: token of this lane's slot row (-1: empty)
-      float dlr[EPI == EPI_GATEDX ? GDX_EMAX : 1];
+      int tok = -1;                 // EPI_SCATTER / EPI_COMBINE: token of this lane's slot row (-1: empty)
+
       float pscale = 0.f;           // EPI_COMBINE: p_t of that token
       if (EPI == EPI_COMBINE) {
         tok = (row_ok && m < p.g.count[b]) ? p.g.tok_of[(size_t)b * p.g.C + m] : -1;
         pscale = tok >= 0 ? p.g.prob[tok] : 0.f;
       }
-      if (EPI == EPI_GATEDX) {
-        tok = (row_ok && m < p.g.count[b]) ? p.g.tok_of[(size_t)b * p.g.C + m] : -1;
-#pragma unroll
-        for (int j = 0; j < GDX_EMAX; j += 4) {
-          float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (tok >= 0 && j < p.g.E) d4 = *reinterpret_cast<const float4*>(p.g.dl + (size_t)tok * p.g.E + j);
-          dlr[j] = d4.x; dlr[j + 1] = d4.y; dlr[j + 2] = d4.z; dlr[j + 3] = d4.w;
-        }
-      }
+      if (EPI == EPI_SCATTER) tok = (row_ok && m < p.g.count[b]) ? p.g.tok_of[(size_t)b * p.g.C + m] : -1;
 #pragma unroll 1
       for (int c = col0; c < col0 + COLS_W; c += 32) {
         const int n = n0 + c;
@@ -491,22 +493,6 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
           } else if (EPI == EPI_COMBINE) {
             o[w] = pack_bf16x2(f.x, f.y);                    // O (slot space, for the backward)
             g[w] = pack_bf16x2(pscale * f.x, pscale * f.y);  // y row of the token
-          } else if (EPI == EPI_GATEDX) {
-            // + sum_j dl[tok][j] Wg[n + 2w (+1)][j] (Wg rows are the same for every lane)
-            float2 gs = f;
-            const float* w0 = p.g.wg + (size_t)(n + 2 * w) * p.g.E;
-#pragma unroll
-            for (int j = 0; j < GDX_EMAX; j += 4) {
-              if (j < p.g.E) {
-                const float4 a = *reinterpret_cast<const float4*>(w0 + j);
-                const float4 c2 = *reinterpret_cast<const float4*>(w0 + p.g.E + j);
-                gs.x = fmaf(dlr[j], a.x, gs.x); gs.x = fmaf(dlr[j + 1], a.y, gs.x);
-                gs.x = fmaf(dlr[j + 2], a.z, gs.x); gs.x = fmaf(dlr[j + 3], a.w, gs.x);
-                gs.y = fmaf(dlr[j], c2.x, gs.y); gs.y = fmaf(dlr[j + 1], c2.y, gs.y);
-                gs.y = fmaf(dlr[j + 2], c2.z, gs.y); gs.y = fmaf(dlr[j + 3], c2.w, gs.y);
-              }
-            }
-            o[w] = pack_bf16x2(gs.x, gs.y);
           } else {
             o[w] = pack_bf16x2(f.x, f.y);
           }
@@ -528,7 +514,7 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
           const bool ok = mm < p.M && col_ok;
           const size_t go = (size_t)b * p.d_bs + (size_t)mm * (size_t)p.N + n + qq * 8;
           const uint4 vd = ld_shared_v4(bD + off);
-          if (EPI == EPI_GATEDX) {  // scatter to the token's dx row
+          if (EPI == EPI_SCATTER) {  // scatter to the token's dx row
             const int trow = __shfl_sync(0xffffffffu, tok, row);
             if (trow >= 0 && col_ok)
               st_v4(static_cast<bf16*>(p.g.dx) + (size_t)trow * p.N + n + qq * 8, vd);
@@ -610,7 +596,8 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
 }
 
 template <int A_MN, int B_MN, int EPI>
-cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
+cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ta2, const CUtensorMap& tb2,
+                    const Params& p, cudaStream_t s) {
   static bool attr = false;
   auto k = gemm2_kernel<A_MN, B_MN, EPI>;
   constexpr int SMEM2_BYTES = smem2_bytes(EPI);
@@ -633,7 +620,7 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const Params& 
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, ta, tb, p);
+  return cudaLaunchKernelEx(&cfg, k, ta, tb, ta2, tb2, p);
 }
 
 }  // namespace
@@ -668,20 +655,29 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
     *why = "combine epilogue needs the CTA-pair kernel";
     return cudaErrorNotSupported;
   }
-  if (a.epilogue == EPI_GATEDX && (!a.gdx || !pair || a.gdx->E > GDX_EMAX || a.gdx->E % 4)) {
-    *why = "gate-dx epilogue needs the CTA-pair kernel and E % 4 == 0, E <= 32";
-    return cudaErrorNotSupported;
+  CUtensorMap ta2 = ta, tb2 = tb;
+  p.k_main = p.k_blocks;
+  if (a.epilogue == EPI_SCATTER) {
+    if (!a.gdx || !pair || !a.b_mn || a.a_mn || !a.gdx->a_ext || !a.gdx->b_ext || a.a_bs || a.d_bs) {
+      *why = "scatter epilogue: CTA-pair kernel, K-major A, MN-major B, extension operands";
+      return cudaErrorNotSupported;
+    }
+    // A2 = [batch][M][64], B2 = [64][N] (one copy, batch coordinate 0)
+    bool ok2 = make_map(&ta2, a.gdx->a_ext, 64, a.M, a.batch, 64, BM) &&
+               make_map(&tb2, a.gdx->b_ext, a.N, 64, 1, 64, 64);
+    if (!ok2) { *why = "cuTensorMapEncodeTiled rejected the extension operands"; return cudaErrorInvalidValue; }
+    p.k_blocks += 1;
   }
   const int key = a.a_mn * 100 + a.b_mn * 10 + a.epilogue;
   if (pair) {
     switch (key) {
-      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, p, s);
-      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, p, s);
-      case 4:   return launch2<0, 0, EPI_COMBINE>(ta, tb, p, s);
-      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, p, s);
-      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, p, s);
-      case 13:  return launch2<0, 1, EPI_GATEDX>(ta, tb, p, s);
-      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, p, s);
+      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, ta, tb, p, s);
+      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, ta, tb, p, s);
+      case 4:   return launch2<0, 0, EPI_COMBINE>(ta, tb, ta, tb, p, s);
+      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, ta, tb, p, s);
+      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, ta, tb, p, s);
+      case 15:  return launch2<0, 1, EPI_SCATTER>(ta, tb, ta2, tb2, p, s);
+      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, ta, tb, p, s);
       default: break;
     }
   } else {

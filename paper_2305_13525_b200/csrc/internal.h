@@ -8,11 +8,12 @@
 namespace moe {
 
 // Batched GEMM D[b] = epi(A[b] . B[b]^T); layouts as in moe.h (moe_gemm_bf16).
-enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_GATEDX = 3, EPI_COMBINE = 4 };
+enum { EPI_STORE = 0, EPI_GELU = 1, EPI_DGELU = 2, EPI_COMBINE = 4, EPI_SCATTER = 5 };
 
-// EPI_GATEDX (B5 on one GPU, top-1, no aux loss): the epilogue adds the gate term of
-// B10 and writes dx rows directly: dx[tok_of[e][c]] = bf16(acc + sum_j dl[t][j] Wg[n][j])
-// for kept slots c < count[e]; empty slots are skipped (E % 4 == 0, E <= 32).
+// EPI_SCATTER (B5 on one GPU, top-1, no aux loss, E <= 16): B10's gate term rides on the
+// tensor cores as one extra 64-wide K block — A_ext[e][c] = [hi(dl_t) | lo(dl_t) | hi(dl_t) | 0]
+// (bf16, t = tok_of[e][c], zeros for empty slots), B_ext = [hi(Wg)^T ; hi(Wg)^T ; lo(Wg)^T ; 0]
+// ([64][H] bf16) — and the epilogue writes dx[tok_of[e][c]] = bf16(acc) for kept slots.
 struct GateDxArgs {
   const int32_t* tok_of;  // [E][C]
   const int32_t* count;   // [E]
@@ -22,6 +23,8 @@ struct GateDxArgs {
   int64_t C;
   void* dx;               // bf16 [T][H] (EPI_COMBINE: y)
   const float* prob;      // EPI_COMBINE: [T] combine weights
+  const void* a_ext;      // EPI_SCATTER: bf16 [E][C][64]
+  const void* b_ext;      // EPI_SCATTER: bf16 [64][H]
 };
 // EPI_COMBINE (F7 on one GPU, top-1): the epilogue stores O as usual and also
 // y[tok_of[e][c]] = bf16(p_t * acc) for kept slots (F11 fused; uses tok_of, count, C,
@@ -115,6 +118,9 @@ int gate_bwd_splits(int64_t T);
 // dropped tokens; dWg = x^T dl (deterministic split-K) after.
 cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* slot, const float* prob,
                     const float* dp, int64_t T, int E, float* dl, cudaStream_t s);
+// EPI_SCATTER extension operands: a_ext [E][C][64] from dl and the slot map, b_ext [64][H] from Wg.
+cudaError_t gate_ext(const float* dl, const int32_t* tok_of, const int32_t* count, const float* wg, int E,
+                     int64_t C, int H, void* a_ext, void* b_ext, cudaStream_t s);
 cudaError_t zero_dropped(const int32_t* slot, int64_t T, int H, void* dx, cudaStream_t s);
 cudaError_t gate_dwg(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,
                      int nsplit, cudaStream_t s);

@@ -132,6 +132,8 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dl = b.take((size_t)d.T * d.E * 4);
   sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));
+  sc->aext = solo ? b.take((size_t)d.E * d.C * 64 * 2) : 0;  // one-GPU fused B5 + B10 (K extension)
+  sc->bext = solo ? b.take((size_t)64 * d.H * 2) : 0;
   sc->dY = d.peer ? 0 : b.take(expert_space);   // peer mode: window WdY
   sc->dO = solo ? sc->dY : (d.peer ? (split ? b.take(slot_space) : 0) : b.take(slot_space));
   sc->dH = b.take(ffn_space);
