@@ -44,7 +44,7 @@ struct GemmArgs {
   // start at A + b * a_bs; of D / aux at D + b * d_bs (a row block of a larger batch,
   // e.g. the rows of one source rank inside [E_l][G_ep][C]). CTA-pair kernel only.
   int64_t a_bs = 0, d_bs = 0;
-  const GateDxArgs* gdx = nullptr;  // EPI_GATEDX only
+  const GateDxArgs* gdx = nullptr;  // EPI_SCATTER / EPI_COMBINE only
 };
 
 // tcgen05 / TMEM / TMA kernel (the product path).
@@ -114,7 +114,7 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
                      const float* aux_f, float aux_coef, cudaStream_t s);
 int gate_bwd_splits(int64_t T);
-// Pieces of B10 for the fused path (EPI_GATEDX): dl [T][E] before B5; zero dx rows of
+// Pieces of B10 for the fused path (EPI_SCATTER): dl [T][E] before B5; zero dx rows of
 // dropped tokens; dWg = x^T dl (deterministic split-K) after.
 cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* slot, const float* prob,
                     const float* dp, int64_t T, int E, float* dl, cudaStream_t s);
