@@ -462,6 +462,7 @@ def main():
 
     if rank == 0:
         out = {"metric": "MoE-layer fwd+bwd tokens/s", "value": value, "unit": "tokens/s",
+               "value_per_gpu": value / world,
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                "data": "synthetic (x, dy ~ N(0,1); Wg ~ N(0,1/H); W1 ~ N(0,1/H); W2 ~ N(0,1/F))",
