@@ -53,9 +53,6 @@ struct moe_ctx {
   void* win[NWIN] = {};
   std::vector<void*> opened;
   void** d_table = nullptr;  // device [world][NWIN]
-  Piece* d_disp = nullptr;
-  Piece* d_ret = nullptr;
-  int n_disp = 0, n_ret = 0;
   std::vector<Piece> h_ret;        // return pieces (host copy, for copy-engine exchanges)
   Piece* d_ret_local = nullptr;    // this rank's own return pieces (SM copy kernel)
   int n_ret_local = 0;
@@ -385,12 +382,6 @@ moe_status setup_peer(moe_ctx* c) {
   CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
-  c->n_disp = (int)disp.size();
-  c->n_ret = (int)ret.size();
-  CUDA_TRY(c, cudaMalloc(&c->d_disp, sizeof(Piece) * (disp.size() + 1)));
-  CUDA_TRY(c, cudaMalloc(&c->d_ret, sizeof(Piece) * (ret.size() + 1)));
-  CUDA_TRY(c, cudaMemcpy(c->d_disp, disp.data(), sizeof(Piece) * disp.size(), cudaMemcpyHostToDevice));
-  CUDA_TRY(c, cudaMemcpy(c->d_ret, ret.data(), sizeof(Piece) * ret.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaMalloc(&c->d_barrier, sizeof(float)));
   CUDA_TRY(c, cudaMemset(c->d_barrier, 0, sizeof(float)));
   CUDA_TRY(c, cudaStreamDestroy(st));
@@ -408,8 +399,6 @@ void teardown_peer(moe_ctx* c) {
   for (int w = 0; w < moe_ctx::NWIN; ++w)
     if (c->win[w]) cudaFree(c->win[w]);
   if (c->d_table) cudaFree(c->d_table);
-  if (c->d_disp) cudaFree(c->d_disp);
-  if (c->d_ret) cudaFree(c->d_ret);
   if (c->d_ret_local) cudaFree(c->d_ret_local);
   if (c->d_barrier) cudaFree(c->d_barrier);
 }
@@ -546,21 +535,6 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
 // Barrier publishing a fused peer write (dispatch / combine-backward) + ledger.
 moe_status publish(moe_ctx* c, bool dispatch, int pass, cudaStream_t st) {
   const Dims& d = c->d;
-  TRY0(barrier(c, st));
-  const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
-  if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
-  if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);
-  return MOE_OK;
-}
-
-// One exchange + the cross-rank barrier that publishes it (every writer's copy
-// kernel precedes its barrier contribution in stream order).
-moe_status exchange(moe_ctx* c, bool dispatch, int pass, const void* src, int win, cudaStream_t st) {
-  const Dims& d = c->d;
-  const size_t pb = (size_t)d.Cs * d.H * 2;
-  CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, dispatch ? c->d_disp : c->d_ret,
-                            dispatch ? c->n_disp : c->n_ret, pb, st));
-  c->stats.kernel_launches[MOE_K_COMM] += 1;
   TRY0(barrier(c, st));
   const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
