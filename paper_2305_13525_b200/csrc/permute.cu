@@ -216,6 +216,11 @@ __global__ void __launch_bounds__(WARPS * 32)
   const bool full = c < count[e];
   const bf16* src = full ? x + (size_t)(tok_of[(size_t)e * ss.C + c] / ss.K) * ss.H : nullptr;
   const int nd = pd.dtd ? pd.Gt : 1;
+  constexpr int MAXD = 8;  // destination rows resolved once per row (G_t <= 8)
+  bf16* dsts[MAXD];
+#pragma unroll
+  for (int k = 0; k < MAXD; ++k)
+    dsts[k] = k < nd ? reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)) : nullptr;
   constexpr int U = 8;
   for (int v0 = 0; v0 < nv; v0 += 32 * U) {
     uint4 buf[U];
@@ -224,12 +229,13 @@ __global__ void __launch_bounds__(WARPS * 32)
       const int v = v0 + u * 32 + lane;
       buf[u] = (full && v < nv) ? ld_nc_v4(src + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
     }
-    for (int k = 0; k < nd; ++k) {
-      bf16* dst = reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t));
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+      if (k >= nd) break;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
-        if (v < nv) st_v4(dst + (size_t)v * 8, buf[u]);
+        if (v < nv) st_v4(dsts[k] + (size_t)v * 8, buf[u]);
       }
     }
   }
@@ -263,6 +269,11 @@ __global__ void __launch_bounds__(WARPS * 32)
   const bf16* orow = O + row;
   const int nv = ss.H / 8;
   const int nd = mine ? (pd.dtd ? pd.Gt : 1) : 0;
+  constexpr int MAXD = 8;
+  bf16* dsts[MAXD];
+#pragma unroll
+  for (int k = 0; k < MAXD; ++k)
+    dsts[k] = k < nd ? reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)) : nullptr;
   float acc = 0.f;
   constexpr int U = 4;
   for (int v0 = 0; v0 < nv; v0 += 32 * U) {
@@ -288,12 +299,13 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
       w[u] = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    for (int k = 0; k < nd; ++k) {
-      bf16* dst = reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t));
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+      if (k >= nd) break;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
-        if (v < nv) st_v4(dst + (size_t)v * 8, w[u]);
+        if (v < nv) st_v4(dsts[k] + (size_t)v * 8, w[u]);
       }
     }
   }
