@@ -359,6 +359,10 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "frac_of_sustained": (achieved / peaks.get('bf16_tflops_sustained', peak)) if achieved else None,
                 "algorithmic_flop_per_launch": gemm_flops_step / 6.0,
+                # padded: every capacity slot computed (empty slots included), SURVEY §8(d)
+                "padded_tflops": (12.0 * H * Fl * El * L["rows_per_expert"]) / (gemm_ms / 1e3) / 1e12
+                if gemm_ms > 0 else None,
+                "frac_of_vendor_2250": (achieved / 2250.0) if achieved else None,
                 "ms_per_launch": gemm_launch_ms, "share_of_step": gemm_ms / ms}
     per_class = {k: v / args.steps for k, v in st["kernel_ms"].items()}
     # HBM-bound steps: algorithmic bytes per step / measured time; slices of the
