@@ -17,11 +17,15 @@
  * for each the F-slice [t*F/G_t, (t+1)*F/G_t): rows of W1 [F,H], columns of
  * W2 [H,F] (Megatron column/row split).
  *
- * World > 1 (default exchange): the library owns peer-visible windows (cudaMalloc,
- * CUDA-IPC mapped on every rank of the box): a ring of MOE_RING = 2 forward windows
- * (expert inputs X and combine sources O) plus one backward pair. A saved blob is
- * valid for backward while at most MOE_RING - 1 newer forwards ran on the ctx
- * (else MOE_ERR_STATE).
+ * World > 1 (default exchange): a communicator (moe_comm) owns peer-visible windows
+ * (cudaMalloc, CUDA-IPC mapped on every rank of the box): a ring of ring_depth
+ * forward windows (expert inputs X and combine sources O) plus the transient
+ * backward / TP-partial windows and a flag page. One communicator serves every MoE
+ * layer of the process (moe_comm_create + moe_create_on_comm), so window memory does
+ * not grow with the number of layers; its size is moe_comm_plan_bytes. moe_create
+ * builds a private communicator for a single layer. Calls of all contexts on one
+ * communicator must be issued in the same order on every rank and stream-ordered
+ * (one stream per rank).
  *
  * Conventions for every call:
  *  - Tensor pointers are caller-owned CUDA device pointers unless stated;
@@ -53,7 +57,10 @@ typedef enum {
   MOE_ERR_STATE = 4,       /* wrong saved blob, poisoned ctx, missing comm         */
   MOE_ERR_CUDA = 5,        /* CUDA runtime / driver error                          */
   MOE_ERR_NCCL = 6,        /* NCCL error                                           */
-  MOE_ERR_UNSUPPORTED = 7  /* valid request this build does not implement         */
+  MOE_ERR_UNSUPPORTED = 7, /* valid request this build does not implement         */
+  MOE_ERR_TIMEOUT = 8      /* a peer rank missed a window barrier / readiness signal
+                              within moe_config.peer_timeout_ms (dead, absent or out
+                              of step); the communicator and its contexts are broken */
 } moe_status;
 
 /* moe_config.flags */
@@ -106,6 +113,16 @@ typedef struct {
                               choices queue behind all first choices); top-2 needs
                               experts >= 2 and no MOE_F_FORCED_ROUTING. With top-2 the
                               per-token routing arrays become [T][2] (expert, slot, prob)  */
+  int32_t ring_depth;      /* world > 1, peer exchange: forwards whose expert inputs X and
+                              combine sources O stay in the communicator's windows until
+                              their backward (0 = 2; at most 64). A saved blob stays valid
+                              for moe_backward while fewer than ring_depth newer forwards
+                              ran on the communicator (else MOE_ERR_STATE). Checkpointed
+                              forwards (MOE_F_CHECKPOINT) take a slot while they run but
+                              stash X/O in `saved`, so their backward needs none. Window
+                              memory is moe_comm_plan_bytes.                              */
+  int32_t peer_timeout_ms; /* deadline of every peer barrier / signal wait (0 = 60000);
+                              a miss surfaces as MOE_ERR_TIMEOUT from the next call       */
 } moe_config;
 
 /* Per-rank derived layout (host-only; no GPU needed). */
@@ -196,6 +213,44 @@ moe_status moe_get_unique_id(uint8_t uid[128]);
  * ctx. */
 moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, int rank,
                       void* scratch, size_t scratch_bytes, moe_ctx** out);
+
+/* ---------------- communicator shared by the layers of a process ----------------
+ *
+ * moe_comm_plan_bytes: device bytes moe_comm_create allocates on this rank for the
+ * layers `cfgs[0..n)` (windows sized for the largest; all layers need the same
+ * g_tensor / g_expert; ring depth and deadline = the largest requested). 0 when no
+ * layer uses the peer exchange (world == 1, or MOE_F_NCCL_EXCHANGE only). NCCL's own
+ * buffers (NCCL-exchange layers only) are not included. Host-only. */
+typedef struct moe_comm moe_comm;
+moe_status moe_comm_plan_bytes(const moe_config* cfgs, int n, int world, int rank, size_t* device_bytes);
+
+/* Collective over the world (world > 1): peer windows exchanged once over a temporary
+ * NCCL communicator (kept only when a layer uses MOE_F_NCCL_EXCHANGE). */
+moe_status moe_comm_create(const moe_config* cfgs, int n, const uint8_t uid[128], int world, int rank,
+                           moe_comm** out);
+/* Destroy after every context created on it (MOE_ERR_STATE otherwise). */
+moe_status moe_comm_destroy(moe_comm* comm);
+
+/* A layer context on a shared communicator (cfg must be one of the configs the
+ * communicator was planned for, or fit in its windows). */
+moe_status moe_create_on_comm(const moe_config* cfg, moe_comm* comm, void* scratch, size_t scratch_bytes,
+                              moe_ctx** out);
+
+/* ---------------- emulated ranks (one process, one device) ----------------
+ * Runs the world > 1 path of every rank of a (g_tensor, g_expert) layout on ONE GPU:
+ * each rank is a host thread with its own stream and its own moe_comm / moe_ctx made by
+ * moe_comm_create_emulated on the group (blocks until all `world` ranks joined). The
+ * ranks' windows are ordinary allocations on the group's device; every exchange,
+ * TP-reduction and combine kernel is the same as with one process per GPU, only the
+ * publication differs: a barrier is a host barrier plus cudaStreamWaitEvent on every
+ * rank's event, a readiness signal is an event (no kernel waits on another kernel).
+ * The NCCL exchange (MOE_F_NCCL_EXCHANGE) cannot be emulated (MOE_ERR_UNSUPPORTED).
+ * Create the group with the device current; destroy it after every rank's comm. */
+typedef struct moe_emu_group moe_emu_group;
+moe_status moe_emu_group_create(int world, moe_emu_group** out);
+moe_status moe_emu_group_destroy(moe_emu_group* group);
+moe_status moe_comm_create_emulated(const moe_config* cfgs, int n, moe_emu_group* group, int rank,
+                                    moe_comm** out);
 
 /* Forward.
  *   x      bf16 [T, H]            tokens of this rank's TP group

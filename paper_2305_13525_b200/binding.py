@@ -40,7 +40,8 @@ class _Config(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
                 ("experts", ctypes.c_int32), ("capacity_factor", ctypes.c_float),
                 ("g_tensor", ctypes.c_int32), ("g_expert", ctypes.c_int32), ("dtd", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("aux_loss_coef", ctypes.c_float), ("top_k", ctypes.c_int32)]
+                ("flags", ctypes.c_uint32), ("aux_loss_coef", ctypes.c_float), ("top_k", ctypes.c_int32),
+                ("ring_depth", ctypes.c_int32), ("peer_timeout_ms", ctypes.c_int32)]
 
 
 class _Layout(ctypes.Structure):
@@ -74,7 +75,11 @@ class _AdamW(ctypes.Structure):
 EXPORTS = ("moe_plan_layout", "moe_plan_bytes", "moe_plan_collectives", "moe_get_unique_id",
            "moe_create", "moe_forward", "moe_backward", "moe_forward_replay", "moe_routing", "moe_stats_get",
            "moe_stats_reset", "moe_destroy", "moe_status_string", "moe_last_error_detail",
-           "moe_gemm_bf16", "moe_adamw_plan", "moe_adamw_step", "moe_aux_loss", "moe_set_priority_seed")
+           "moe_gemm_bf16", "moe_adamw_plan", "moe_adamw_step", "moe_aux_loss", "moe_set_priority_seed",
+           "moe_comm_plan_bytes", "moe_comm_create", "moe_comm_destroy", "moe_create_on_comm",
+           "moe_emu_group_create", "moe_emu_group_destroy", "moe_comm_create_emulated")
+MOE_ERR_STATE = 4
+MOE_ERR_TIMEOUT = 8
 
 _lib = None
 
@@ -111,6 +116,13 @@ def lib() -> ctypes.CDLL:
     L.moe_set_priority_seed.argtypes = [P, ctypes.c_uint64]
     L.moe_adamw_plan.argtypes = [I64, I64, ctypes.POINTER(I64), ctypes.POINTER(SZ)]
     L.moe_adamw_step.argtypes = [P, P, P, P, P, I64, ctypes.POINTER(_AdamW), I64, P, P]
+    L.moe_comm_plan_bytes.argtypes = [cfgp, I, I, I, ctypes.POINTER(SZ)]
+    L.moe_comm_create.argtypes = [cfgp, I, ctypes.c_char_p, I, I, ctypes.POINTER(P)]
+    L.moe_comm_destroy.argtypes = [P]
+    L.moe_create_on_comm.argtypes = [cfgp, P, P, SZ, ctypes.POINTER(P)]
+    L.moe_emu_group_create.argtypes = [I, ctypes.POINTER(P)]
+    L.moe_emu_group_destroy.argtypes = [P]
+    L.moe_comm_create_emulated.argtypes = [cfgp, I, P, I, ctypes.POINTER(P)]
     for name in EXPORTS:
         if name not in ("moe_status_string", "moe_last_error_detail"):
             getattr(L, name).restype = ctypes.c_int
@@ -137,11 +149,17 @@ class MoEConfig:
     flags: int = MOE_F_STATS
     aux_loss_coef: float = 0.0
     top_k: int = 1
+    ring_depth: int = 0          # 0 = 2 forwards in flight per communicator
+    peer_timeout_ms: int = 0     # 0 = 60 s deadline per peer barrier / signal wait
 
     def c(self) -> _Config:
         return _Config(self.tokens, self.hidden, self.ffn, self.experts, self.capacity_factor,
                        self.g_tensor, self.g_expert, int(self.dtd), self.flags, self.aux_loss_coef,
-                       self.top_k)
+                       self.top_k, self.ring_depth, self.peer_timeout_ms)
+
+    def replace(self, **kw) -> "MoEConfig":
+        import dataclasses
+        return dataclasses.replace(self, **kw)
 
     @staticmethod
     def from_shape(shape, dtd: bool = True, forced: bool = False, tokens: int | None = None):
@@ -171,6 +189,60 @@ def moe_plan_collectives(cfg: MoEConfig, world: int = 1, rank: int = 0) -> list[
     return [{"kind": COLL_NAMES[a.kind], "pass": ("forward", "backward", "replay")[a.pass_], "step": a.step,
              "group_size": a.group_size, "buffer_bytes": a.buffer_bytes, "wire_bytes": a.wire_bytes}
             for a in arr[:n.value]]
+
+
+def _cfg_array(cfgs):
+    cfgs = list(cfgs)
+    arr = (_Config * len(cfgs))(*[c.c() for c in cfgs])
+    return arr, len(cfgs)
+
+
+def moe_comm_plan_bytes(cfgs, world: int, rank: int = 0) -> int:
+    """Device bytes of the peer windows a communicator for these layers allocates."""
+    arr, n = _cfg_array(cfgs)
+    out = ctypes.c_size_t()
+    _check(lib().moe_comm_plan_bytes(arr, n, world, rank, ctypes.byref(out)))
+    return out.value
+
+
+class MoEComm:
+    """A communicator shared by the MoE layers of one process (moe_comm_create), or one
+    rank of an emulated group (EmuGroup.comm). Layers attach with MoELayer(..., comm=)."""
+
+    def __init__(self, cfgs, world: int, rank: int, emu: "EmuGroup | None" = None):
+        self.world, self.rank = world, rank
+        self.cfgs = list(cfgs)
+        arr, n = _cfg_array(self.cfgs)
+        h = ctypes.c_void_p()
+        if emu is not None:
+            _check(lib().moe_comm_create_emulated(arr, n, emu.h, rank, ctypes.byref(h)))
+        else:
+            import torch.distributed as dist
+            obj = [moe_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            _check(lib().moe_comm_create(arr, n, obj[0], world, rank, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            _check(lib().moe_comm_destroy(self.h))
+            self.h = ctypes.c_void_p()
+
+
+class EmuGroup:
+    """`world` ranks emulated in this process on the current device (moe_emu_group):
+    every rank runs on its own Python thread and stream (ctypes releases the GIL)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        h = ctypes.c_void_p()
+        _check(lib().moe_emu_group_create(world, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().moe_emu_group_destroy(self.h)
+            self.h = ctypes.c_void_p()
 
 
 def moe_get_unique_id() -> bytes:
@@ -226,13 +298,23 @@ class MoELayer:
     (the default process group, any backend) before moe_create.
     """
 
-    def __init__(self, cfg: MoEConfig, world: int = 1, rank: int = 0, device=None):
+    def __init__(self, cfg: MoEConfig, world: int = 1, rank: int = 0, device=None,
+                 comm: MoEComm | None = None):
         self.cfg = cfg
+        if comm is not None:
+            world, rank = comm.world, comm.rank
         self.world, self.rank = world, rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.layout = moe_plan_layout(cfg, world, rank)
         self.saved_bytes, self.scratch_bytes = moe_plan_bytes(cfg, world, rank)
         self.scratch = torch.empty(max(self.scratch_bytes, 256), dtype=torch.uint8, device=self.device)
+        self.comm = comm
+        if comm is not None:
+            ctx = ctypes.c_void_p()
+            _check(lib().moe_create_on_comm(ctypes.byref(cfg.c()), comm.h, _ptr(self.scratch),
+                                            self.scratch_bytes, ctypes.byref(ctx)))
+            self.ctx = ctx
+            return
         uid = bytes(128)
         if world > 1:
             import torch.distributed as dist

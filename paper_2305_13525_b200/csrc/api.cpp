@@ -24,6 +24,7 @@
 #include "../../include/moe.h"
 #include "../../include/moe_optim.h"
 #include "internal.h"
+#include "comm.h"
 #include "plan.h"
 
 using namespace moe;
@@ -35,37 +36,23 @@ struct moe_ctx {
   ScratchLayout sc;
   uint8_t* scratch = nullptr;
   size_t scratch_bytes = 0;
-  ncclComm_t world_comm = nullptr, tp_comm = nullptr, ep_comm = nullptr;
+  moe_comm* comm = nullptr;  // world > 1: windows, ring, NCCL communicators (comm.h)
   bool poisoned = false;
   uint64_t priority_seed = 0;  // MOE_F_RANDOM_PRIORITY key (moe_set_priority_seed)
   bool no_fused_dx = false;    // MOE_NO_FUSED_DX=1: B10 as a separate kernel (A/B, tests)
   bool no_fused_combine = false;  // MOE_NO_FUSED_COMBINE=1: F11 as a separate kernel
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
-  // peer-memory exchange (d.peer): library-owned, IPC-mapped windows
-  // W_Y / W_DXP: the TP partials of GEMM2 / B5, read by the TP partners (G_t > 1)
-  enum { W_X0 = 0, W_X1 = 1, W_O0 = 2, W_O1 = 3, W_DY = 4, W_DS = 5, W_FLAGS = 6, W_Y = 7, W_DXP = 8,
-         NWIN = 9 };
-  // W_FLAGS: barrier slots [0, world), per-source readiness slots from SIG_OFF
-  enum { SIG_OFF = 4096 };
-  uint32_t sig_epoch = 0;
-  uint32_t epoch = 0;  // flag-barrier epoch
-  void* win[NWIN] = {};
-  std::vector<void*> opened;
-  void** d_table = nullptr;  // device [world][NWIN]
+  // peer-memory exchange (d.peer): this layer's piece lists over the comm's windows
   std::vector<Piece> h_ret;        // return pieces (host copy, for copy-engine exchanges)
-  Piece* d_ret_local = nullptr;    // this rank's own return pieces (SM copy kernel)
+  Piece* d_ret_local = nullptr;    // this rank's own return pieces (SM copy kernel; comm arena)
   int n_ret_local = 0;
   std::vector<int> h_ret_el;       // local expert of each return piece
-  std::vector<void*> h_table;      // [world][NWIN] peer-mapped pointers
   cudaStream_t side = nullptr;     // copy-engine / overlap stream
   bool overlap = true;             // MOE_NO_OVERLAP=1: serial return exchanges (A/B knob)
   cudaEvent_t ev[4] = {};
   cudaEvent_t evp[4] = {};  // GEMM2 parts (G_t = 1 return overlap)
   int64_t disp_bytes[3] = {0, 0, 0}, ret_bytes[3] = {0, 0, 0};  // by Piece::kind
-  float* d_barrier = nullptr;
-  uint64_t gen = 0;
-  uint64_t ring_gen[2] = {0, 0};
   std::unordered_map<const void*, std::pair<int, uint64_t>> saved_slot;  // saved -> (ring slot, gen)
   const void* replayed = nullptr;  // MOE_F_CHECKPOINT: saved blob whose G/A sit in scratch
   const void* last_saved = nullptr;
@@ -190,11 +177,11 @@ moe_status ep_exchange(moe_ctx* c, int dir, int pass, void* S, void* X, int lo, 
     for (int el = 0; el < d.El; ++el)
       for (int tt = lo; tt < hi; ++tt) {
         if (dir == 0) {
-          NCCL_TRY(c, ncclSend(s_at(tt, p * d.El + el), piece, ncclBfloat16, p, c->ep_comm, st));
-          NCCL_TRY(c, ncclRecv(x_at(el, tt, p), piece, ncclBfloat16, p, c->ep_comm, st));
+          NCCL_TRY(c, ncclSend(s_at(tt, p * d.El + el), piece, ncclBfloat16, p, c->comm->ep_comm, st));
+          NCCL_TRY(c, ncclRecv(x_at(el, tt, p), piece, ncclBfloat16, p, c->comm->ep_comm, st));
         } else {
-          NCCL_TRY(c, ncclSend(x_at(el, tt, p), piece, ncclBfloat16, p, c->ep_comm, st));
-          NCCL_TRY(c, ncclRecv(s_at(tt, p * d.El + el), piece, ncclBfloat16, p, c->ep_comm, st));
+          NCCL_TRY(c, ncclSend(x_at(el, tt, p), piece, ncclBfloat16, p, c->comm->ep_comm, st));
+          NCCL_TRY(c, ncclRecv(s_at(tt, p * d.El + el), piece, ncclBfloat16, p, c->comm->ep_comm, st));
         }
       }
   }
@@ -210,7 +197,7 @@ moe_status ag_expert(moe_ctx* c, int pass, void* X, cudaStream_t st) {
   NCCL_TRY(c, ncclGroupStart());
   for (int el = 0; el < d.El; ++el) {
     uint8_t* base = at<uint8_t>(X, (size_t)el * d.R * d.H * 2);
-    NCCL_TRY(c, ncclAllGather(base + (size_t)d.t * cnt * 2, base, cnt, ncclBfloat16, c->tp_comm, st));
+    NCCL_TRY(c, ncclAllGather(base + (size_t)d.t * cnt * 2, base, cnt, ncclBfloat16, c->comm->tp_comm, st));
   }
   NCCL_TRY(c, ncclGroupEnd());
   const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
@@ -228,7 +215,7 @@ moe_status rs_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st, int el_lo =
   for (int el = el_lo; el < el_hi; ++el) {
     uint8_t* base = at<uint8_t>(Y, (size_t)el * d.R * d.H * 2);
     NCCL_TRY(c, ncclReduceScatter(base, base + (size_t)d.t * cnt * 2, cnt, ncclBfloat16, ncclSum,
-                                  c->tp_comm, st));
+                                  c->comm->tp_comm, st));
   }
   NCCL_TRY(c, ncclGroupEnd());
   const int64_t xe = (int64_t)d.El * d.R * d.H * 2;
@@ -243,7 +230,7 @@ moe_status ar_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st, int el_lo =
   if (el_hi < 0) el_hi = d.El;
   const size_t per = (size_t)d.R * d.H;
   uint8_t* base = at<uint8_t>(Y, (size_t)el_lo * per * 2);
-  NCCL_TRY(c, ncclAllReduce(base, base, per * (el_hi - el_lo), ncclBfloat16, ncclSum, c->tp_comm, st));
+  NCCL_TRY(c, ncclAllReduce(base, base, per * (el_hi - el_lo), ncclBfloat16, ncclSum, c->comm->tp_comm, st));
   const size_t cnt = (size_t)d.El * per;
   if (count) ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * (int64_t)cnt * 2 * (d.Gt - 1) / d.Gt);
   return MOE_OK;
@@ -253,7 +240,7 @@ moe_status ar_expert(moe_ctx* c, int pass, void* Y, cudaStream_t st, int el_lo =
 moe_status ag_slot(moe_ctx* c, int pass, void* O, cudaStream_t st) {
   const Dims& d = c->d;
   const size_t cnt = (size_t)d.E * d.Cs * d.H;
-  NCCL_TRY(c, ncclAllGather(at<uint8_t>(O, (size_t)d.t * cnt * 2), O, cnt, ncclBfloat16, c->tp_comm, st));
+  NCCL_TRY(c, ncclAllGather(at<uint8_t>(O, (size_t)d.t * cnt * 2), O, cnt, ncclBfloat16, c->comm->tp_comm, st));
   ledger(c, MOE_COLL_ALLGATHER, pass, (int64_t)d.E * d.C * d.H * 2 * (d.Gt - 1) / d.Gt);
   return MOE_OK;
 }
@@ -328,90 +315,60 @@ void build_pieces(const Dims& d, bool dispatch, std::vector<Piece>& v, int64_t b
   }
 }
 
+// Per-layer exchange state over the communicator's windows: piece lists (the local
+// return pieces live in the comm's device arena), the overlap stream and its events.
 moe_status setup_peer(moe_ctx* c) {
   const Dims& d = c->d;
-  const size_t expert_space = (size_t)d.El * d.R * d.H * 2;
-  const size_t slot_space = (size_t)d.E * d.C * d.H * 2;
-  const size_t tp_space = d.Gt > 1 ? expert_space : 256;
-  const size_t sizes[moe_ctx::NWIN] = {expert_space, expert_space, slot_space, slot_space,
-                                       expert_space, slot_space, (size_t)moe_ctx::SIG_OFF + 4 * (size_t)d.world,
-                                       tp_space, tp_space};
-  std::vector<cudaIpcMemHandle_t> mine(moe_ctx::NWIN);
-  for (int w = 0; w < moe_ctx::NWIN; ++w) {
-    CUDA_TRY(c, cudaMalloc(&c->win[w], sizes[w]));
-    CUDA_TRY(c, cudaMemset(c->win[w], 0, sizes[w]));
-    CUDA_TRY(c, cudaIpcGetMemHandle(&mine[w], c->win[w]));
-  }
-  const size_t hb = sizeof(cudaIpcMemHandle_t) * moe_ctx::NWIN;
-  uint8_t* dbuf = nullptr;
-  CUDA_TRY(c, cudaMalloc(&dbuf, hb * d.world));
-  CUDA_TRY(c, cudaMemcpy(dbuf + hb * d.rank, mine.data(), hb, cudaMemcpyHostToDevice));
-  cudaStream_t st;
-  CUDA_TRY(c, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  NCCL_TRY(c, ncclAllGather(dbuf + hb * d.rank, dbuf, hb, ncclUint8, c->world_comm, st));
-  CUDA_TRY(c, cudaStreamSynchronize(st));
-  std::vector<cudaIpcMemHandle_t> all(moe_ctx::NWIN * d.world);
-  CUDA_TRY(c, cudaMemcpy(all.data(), dbuf, hb * d.world, cudaMemcpyDeviceToHost));
-  cudaFree(dbuf);
-  std::vector<void*> table((size_t)d.world * moe_ctx::NWIN, nullptr);
-  for (int r = 0; r < d.world; ++r)
-    for (int w = 0; w < moe_ctx::NWIN; ++w) {
-      if (r == d.rank) {
-        table[(size_t)r * moe_ctx::NWIN + w] = c->win[w];
-        continue;
-      }
-      void* p = nullptr;
-      CUDA_TRY(c, cudaIpcOpenMemHandle(&p, all[(size_t)r * moe_ctx::NWIN + w],
-                                       cudaIpcMemLazyEnablePeerAccess));
-      c->opened.push_back(p);
-      table[(size_t)r * moe_ctx::NWIN + w] = p;
-    }
-  CUDA_TRY(c, cudaMalloc(&c->d_table, sizeof(void*) * table.size()));
-  CUDA_TRY(c, cudaMemcpy(c->d_table, table.data(), sizeof(void*) * table.size(), cudaMemcpyHostToDevice));
+  moe_comm* m = c->comm;
   std::vector<Piece> disp, ret;
   build_pieces(d, true, disp, c->disp_bytes);
   build_pieces(d, false, ret, c->ret_bytes, &c->h_ret_el);
   c->h_ret = ret;
-  c->h_table = table;
   std::vector<Piece> loc;
   for (const Piece& p : ret)
     if (p.dst_rank == d.rank) loc.push_back(p);
   c->n_ret_local = (int)loc.size();
-  CUDA_TRY(c, cudaMalloc(&c->d_ret_local, sizeof(Piece) * (loc.size() + 1)));
-  CUDA_TRY(c, cudaMemcpy(c->d_ret_local, loc.data(), sizeof(Piece) * loc.size(), cudaMemcpyHostToDevice));
+  c->d_ret_local = comm_pieces(m, (int)loc.size());
+  if (!c->d_ret_local) return fail(MOE_ERR_STATE, "communicator piece arena exhausted (too many layers)");
+  if (!loc.empty())
+    CUDA_TRY(c, cudaMemcpy(c->d_ret_local, loc.data(), sizeof(Piece) * loc.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
-  CUDA_TRY(c, cudaMalloc(&c->d_barrier, sizeof(float)));
-  CUDA_TRY(c, cudaMemset(c->d_barrier, 0, sizeof(float)));
-  CUDA_TRY(c, cudaStreamDestroy(st));
   return MOE_OK;
 }
 
 void teardown_peer(moe_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
+  c->side = nullptr;
   for (int i = 0; i < 4; ++i) {
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->evp[i]) cudaEventDestroy(c->evp[i]);
+    c->ev[i] = c->evp[i] = nullptr;
   }
-  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
-  c->opened.clear();
-  for (int w = 0; w < moe_ctx::NWIN; ++w)
-    if (c->win[w]) cudaFree(c->win[w]);
-  if (c->d_table) cudaFree(c->d_table);
-  if (c->d_ret_local) cudaFree(c->d_ret_local);
-  if (c->d_barrier) cudaFree(c->d_barrier);
 }
 
 PeerDst peer_dst(const moe_ctx* c, int win) {
   const Dims& d = c->d;
   PeerDst pd;
-  pd.table = c->d_table;
-  pd.nwin = moe_ctx::NWIN;
+  pd.table = c->comm->d_table;
+  pd.nwin = c->comm->nwin;
   pd.win = win;
   pd.d = d.d; pd.ep = d.ep; pd.t = d.t; pd.Gt = d.Gt; pd.Gep = d.Gep; pd.El = d.El;
   pd.dtd = d.dtd ? 1 : 0;
   return pd;
+}
+
+// A deadline failure of the communicator (device-side spin or emulated host barrier)
+// poisons the context and is reported as MOE_ERR_TIMEOUT.
+moe_status check_comm(moe_ctx* c) {
+  std::string why;
+  const moe_status s = comm_check(c->comm, &why);
+  if (s != MOE_OK) {
+    c->poisoned = true;
+    return fail(s, why);
+  }
+  return MOE_OK;
 }
 
 #define TRY0(expr)                        \
@@ -432,7 +389,7 @@ moe_status exchange_ce(moe_ctx* c, const void* src, int win, int el_lo, int el_h
     if (el < el_lo || el >= el_hi) continue;
     const Piece& p = c->h_ret[i];
     if (p.dst_rank == d.rank) continue;
-    uint8_t* dst = static_cast<uint8_t*>(c->h_table[(size_t)p.dst_rank * moe_ctx::NWIN + win]) + p.dst_off;
+    uint8_t* dst = static_cast<uint8_t*>(c->comm->h_table[(size_t)p.dst_rank * c->comm->nwin + win]) + p.dst_off;
     CUDA_TRY(c, cudaMemcpyAsync(dst, static_cast<const uint8_t*>(src) + p.src_off, pb,
                                 cudaMemcpyDeviceToDevice, st));
   }
@@ -447,32 +404,34 @@ moe_status exchange_ce(moe_ctx* c, const void* src, int win, int el_lo, int el_h
 // readiness flag in that destination's flag region; returns the epoch to wait for.
 moe_status exchange_ce_dispatch_sig(moe_ctx* c, const void* stage, int win, cudaStream_t st, uint32_t* epoch) {
   const Dims& d = c->d;
+  moe_comm* m = c->comm;
   const size_t pb = (size_t)d.C * d.H * 2;
-  const uint32_t ep = ++c->sig_epoch;
+  const uint32_t ep = ++m->sig_epoch;
   *epoch = ep;
   for (int k = 1; k < d.Gep; ++k) {
     const int ep2 = (d.ep + k) % d.Gep;
     const int r = d.d * d.Gep + ep2;  // G_t = 1
     for (int el = 0; el < d.El; ++el) {
       const uint8_t* src = static_cast<const uint8_t*>(stage) + (size_t)(ep2 * d.El + el) * pb;
-      uint8_t* dst = static_cast<uint8_t*>(c->h_table[(size_t)r * moe_ctx::NWIN + win]) +
+      uint8_t* dst = static_cast<uint8_t*>(m->h_table[(size_t)r * m->nwin + win]) +
                      ((size_t)el * d.Gep + d.ep) * pb;
       CUDA_TRY(c, cudaMemcpyAsync(dst, src, pb, cudaMemcpyDeviceToDevice, st));
     }
-    uint32_t* flag = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(
-        c->h_table[(size_t)r * moe_ctx::NWIN + moe_ctx::W_FLAGS]) + moe_ctx::SIG_OFF) + d.ep;
-    CUDA_TRY(c, peer_signal(flag, ep, st));
-    c->stats.kernel_launches[MOE_K_COMM] += 1;
+    std::string why;
+    const moe_status s = comm_signal(m, r, ep, st, &why);
+    if (s != MOE_OK) { c->poisoned = true; return fail(s, why); }
+    if (m->tr == TR_IPC) c->stats.kernel_launches[MOE_K_COMM] += 1;
   }
   return MOE_OK;
 }
 
 // Waits (on st) until source block `src`'s pieces of exchange `epoch` are in this rank's window.
 moe_status wait_source(moe_ctx* c, int src, uint32_t epoch, cudaStream_t st) {
-  const uint32_t* flag = reinterpret_cast<const uint32_t*>(
-      static_cast<uint8_t*>(c->win[moe_ctx::W_FLAGS]) + moe_ctx::SIG_OFF) + src;
-  CUDA_TRY(c, peer_wait(flag, epoch, st));
-  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  moe_comm* m = c->comm;
+  std::string why;
+  const moe_status s = comm_wait(m, c->d.d * c->d.Gep + src, epoch, st, &why);  // G_t = 1: rank = d*G_ep + ep
+  if (s != MOE_OK) { c->poisoned = true; return fail(s, why); }
+  if (m->tr == TR_IPC) c->stats.kernel_launches[MOE_K_COMM] += 1;
   return MOE_OK;
 }
 
@@ -497,16 +456,17 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
 
 moe_status exchange_local(moe_ctx* c, const void* src, int win, cudaStream_t st) {
   const Dims& d = c->d;
-  CUDA_TRY(c, peer_exchange(src, c->d_table, moe_ctx::NWIN, win, c->d_ret_local, c->n_ret_local,
+  CUDA_TRY(c, peer_exchange(src, c->comm->d_table, c->comm->nwin, win, c->d_ret_local, c->n_ret_local,
                             (size_t)d.Cs * d.H * 2, st));
   c->stats.kernel_launches[MOE_K_COMM] += 1;
   return MOE_OK;
 }
 
 moe_status barrier(moe_ctx* c, cudaStream_t st) {
-  const Dims& d = c->d;
-  CUDA_TRY(c, peer_barrier(c->d_table, moe_ctx::NWIN, moe_ctx::W_FLAGS, d.world, d.rank, ++c->epoch, st));
-  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  std::string why;
+  const moe_status s = comm_barrier(c->comm, st, &why);
+  if (s != MOE_OK) { c->poisoned = true; return fail(s, why); }
+  if (c->comm->tr == TR_IPC) c->stats.kernel_launches[MOE_K_COMM] += 1;
   return MOE_OK;
 }
 
@@ -514,8 +474,8 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
   const Dims& d = c->d;
   TRY0(barrier(c, st));
   ReduceReturn rr;
-  rr.table = c->d_table;
-  rr.nwin = moe_ctx::NWIN;
+  rr.table = c->comm->d_table;
+  rr.nwin = c->comm->nwin;
   rr.src_win = src_win;
   rr.dst_win = dst_win;
   rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E; rr.H = d.H;
@@ -562,7 +522,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   const bool solo = d.world == 1;
   const int lo = d.dtd ? d.t : 0, hi = d.dtd ? d.t + 1 : d.Gt;
   // F3 dispatch (DTD: only this rank's slot slice), F4 a2a, F5 all-gather
-  void* X = d.peer ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
+  void* X = d.peer ? c->comm->win[c->comm->wx(rslot)] : at<uint8_t>(saved, sv.X);
   const int32_t* tok_of = at<int32_t>(saved, sv.tok_of);
   const int32_t* count = at<int32_t>(saved, sv.count);
   void* D = sc.D_in_saved ? X : at<uint8_t>(c->scratch, sc.D);
@@ -581,14 +541,14 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
     {
       Scope sx_(c, MOE_K_XFER, c->side, 0);
-      TRY(exchange_ce_dispatch_sig(c, D, moe_ctx::W_X0 + rslot, c->side, &sig));
+      TRY(exchange_ce_dispatch_sig(c, D, c->comm->wx(rslot), c->side, &sig));
     }
     ledger(c, MOE_COLL_A2A, pass, c->disp_bytes[1]);
   } else if (d.peer) {
     // fused: rows go straight from x into the peers' expert-space windows
     {
       Scope sc_(c, MOE_K_DISPATCH, st, 1);
-      CUDA_TRY(c, dispatch_peer(x, tok_of, count, ss, lo, hi, peer_dst(c, moe_ctx::W_X0 + rslot), st));
+      CUDA_TRY(c, dispatch_peer(x, tok_of, count, ss, lo, hi, peer_dst(c, c->comm->wx(rslot)), st));
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, pass, st));
@@ -612,8 +572,8 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   // F6 GEMM1 + GeLU (stores A = gelu(Hpre) and G = gelu'(Hpre)), F7 GEMM2
   void* G = d.ckpt ? at<uint8_t>(c->scratch, sc.Grec) : at<uint8_t>(saved, sv.G);
   void* A = d.ckpt ? at<uint8_t>(c->scratch, sc.Arec) : at<uint8_t>(saved, sv.A);
-  void* O = d.peer ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
-  void* Y = sc.Y_in_saved ? O : (d.peer && d.Gt > 1 ? c->win[moe_ctx::W_Y] : at<uint8_t>(c->scratch, sc.Ypart));
+  void* O = d.peer ? c->comm->win[c->comm->wo(rslot)] : at<uint8_t>(saved, sv.O);
+  void* Y = sc.Y_in_saved ? O : (d.peer && d.Gt > 1 ? c->comm->win[moe_comm::W_Y] : at<uint8_t>(c->scratch, sc.Ypart));
   GemmArgs g1{d.El, (int)d.R, d.Fl, d.H, X, 0, w1, 0, G, EPI_GELU, A};
   if (split) {
     // own block first (already in place), then each source block as its pieces land
@@ -641,7 +601,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
     TRY(gemm(c, g2, st));
     Scope sc_(c, MOE_K_COMM, st, 0);
-    TRY(tp_return(c, pass, moe_ctx::W_Y, moe_ctx::W_O0 + rslot, st));
+    TRY(tp_return(c, pass, moe_comm::W_Y, c->comm->wo(rslot), st));
     if (d.ckpt) {  // CAC stash of the second collective's output
       CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.O), O, (size_t)d.E * d.C * d.H * 2,
                                   cudaMemcpyDeviceToDevice, st));
@@ -664,13 +624,13 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
       CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->evp[part], 0));
       {
         Scope sx_(c, MOE_K_XFER, c->side, 0);
-        TRY(exchange_ce(c, Y, moe_ctx::W_O0 + rslot, e0, e1, c->side));
+        TRY(exchange_ce(c, Y, c->comm->wo(rslot), e0, e1, c->side));
       }
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[2], c->side));
     Scope sc_(c, MOE_K_COMM, st, 0);
     CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[2], 0));
-    TRY(exchange_local(c, Y, moe_ctx::W_O0 + rslot, st));
+    TRY(exchange_local(c, Y, c->comm->wo(rslot), st));
     TRY(barrier(c, st));
     if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
     if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
@@ -725,6 +685,7 @@ const char* moe_status_string(moe_status s) {
     case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
     case MOE_ERR_NCCL: return "MOE_ERR_NCCL";
     case MOE_ERR_UNSUPPORTED: return "MOE_ERR_UNSUPPORTED";
+    case MOE_ERR_TIMEOUT: return "MOE_ERR_TIMEOUT";
   }
   return "MOE_ERR_UNKNOWN";
 }
@@ -781,10 +742,13 @@ moe_status moe_get_unique_id(uint8_t uid[128]) {
   return MOE_OK;
 }
 
-moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, int rank,
-                      void* scratch, size_t scratch_bytes, moe_ctx** out) {
-  if (!out) return fail(MOE_ERR_ARG, "null ctx output");
-  *out = nullptr;
+}  // extern "C"
+
+namespace {
+
+// A layer context on communicator m (nullptr when world == 1).
+moe_status make_ctx(const moe_config* cfg, moe_comm* m, int world, int rank, void* scratch,
+                    size_t scratch_bytes, moe_ctx** out) {
   Dims d;
   std::string why;
   moe_status s = make_dims(cfg, world, rank, &d, &why);
@@ -795,6 +759,8 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
     c->no_fused_dx = nf && nf[0] == '1';
     const char* nc = std::getenv("MOE_NO_FUSED_COMBINE");
     c->no_fused_combine = nc && nc[0] == '1';
+    const char* no = std::getenv("MOE_NO_OVERLAP");
+    c->overlap = !(no && no[0] == '1');
   }
   c->d = d;
   c->cfg = *cfg;
@@ -812,46 +778,125 @@ moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, 
   c->scratch = static_cast<uint8_t*>(scratch);
   c->scratch_bytes = scratch_bytes;
   if (world > 1) {
-    if (!uid) { delete c; return fail(MOE_ERR_ARG, "uid required when world > 1"); }
-    ncclUniqueId id;
-    std::memcpy(&id, uid, 128);
-    ncclResult_t r = ncclCommInitRank(&c->world_comm, world, id, rank);
-    if (r != ncclSuccess) { delete c; return fail(MOE_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); }
-    r = ncclCommSplit(c->world_comm, d.d * d.Gep + d.ep, d.t, &c->tp_comm, nullptr);
-    if (r == ncclSuccess) r = ncclCommSplit(c->world_comm, d.d * d.Gt + d.t, d.ep, &c->ep_comm, nullptr);
-    if (r != ncclSuccess) {
-      ncclCommDestroy(c->world_comm);
-      delete c;
-      return fail(MOE_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
-    }
-    if (d.peer) {
-      const char* no = std::getenv("MOE_NO_OVERLAP");
-      c->overlap = !(no && no[0] == '1');
-      moe_status ps = setup_peer(c);
-      if (ps != MOE_OK) {
-        const std::string why2 = g_detail;
-        teardown_peer(c);
-        if (c->tp_comm) ncclCommDestroy(c->tp_comm);
-        if (c->ep_comm) ncclCommDestroy(c->ep_comm);
-        ncclCommDestroy(c->world_comm);
-        delete c;
-        return fail(ps, "peer-memory exchange setup: " + why2);
+    // the layer must fit the communicator it is attached to
+    CommPlan need;
+    s = make_comm_plan(cfg, 1, world, rank, &need, &why);
+    const CommPlan& have = m->plan;
+    if (s == MOE_OK) {
+      if (have.world != world || have.rank != rank || have.Gt != d.Gt || have.Gep != d.Gep) {
+        s = MOE_ERR_ARG;
+        why = "layer's world/rank/g_tensor/g_expert differ from the communicator's";
+      } else if (need.peer && (!have.peer || need.expert_space > have.expert_space ||
+                               need.slot_space > have.slot_space || need.tp_space > have.tp_space)) {
+        s = MOE_ERR_ARG;
+        why = "layer needs larger peer windows than the communicator was planned for";
+      } else if (need.nccl && !m->tp_comm) {
+        s = MOE_ERR_STATE;
+        why = "MOE_F_NCCL_EXCHANGE layer on a communicator planned without it";
       }
     }
+    if (s != MOE_OK) { delete c; return fail(s, why); }
+    c->comm = m;
+    if (d.peer) {
+      s = setup_peer(c);
+      if (s != MOE_OK) {
+        const std::string why2 = g_detail;
+        teardown_peer(c);
+        delete c;
+        return fail(s, "peer-memory exchange setup: " + why2);
+      }
+    }
+    m->refs += 1;
   }
   *out = c;
   return MOE_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+moe_status moe_comm_plan_bytes(const moe_config* cfgs, int n, int world, int rank, size_t* device_bytes) {
+  if (!device_bytes) return fail(MOE_ERR_ARG, "null output");
+  CommPlan p;
+  std::string why;
+  moe_status s = make_comm_plan(cfgs, n, world, rank, &p, &why);
+  if (s != MOE_OK) return fail(s, why);
+  *device_bytes = p.total;
+  return MOE_OK;
+}
+
+moe_status moe_comm_create(const moe_config* cfgs, int n, const uint8_t uid[128], int world, int rank,
+                           moe_comm** out) {
+  if (!out) return fail(MOE_ERR_ARG, "null comm output");
+  if (world < 2) return fail(MOE_ERR_ARG, "a communicator needs world > 1");
+  std::string why;
+  moe_status s = comm_create(cfgs, n, uid, nullptr, world, rank, out, &why);
+  if (s != MOE_OK) return fail(s, why);
+  return MOE_OK;
+}
+
+moe_status moe_comm_create_emulated(const moe_config* cfgs, int n, moe_emu_group* group, int rank,
+                                    moe_comm** out) {
+  if (!out || !group) return fail(MOE_ERR_ARG, "null group / comm output");
+  int world = 0;
+  world = emu_world(group);
+  moe_status s;
+  if (world < 2) return fail(MOE_ERR_ARG, "an emulated group needs world > 1");
+  std::string why;
+  s = comm_create(cfgs, n, nullptr, group, world, rank, out, &why);
+  if (s != MOE_OK) return fail(s, why);
+  return MOE_OK;
+}
+
+moe_status moe_comm_destroy(moe_comm* m) {
+  if (!m) return MOE_OK;
+  if (m->refs > 0) return fail(MOE_ERR_STATE, "layer contexts still attached to the communicator");
+  cudaDeviceSynchronize();
+  comm_destroy(m);
+  return MOE_OK;
+}
+
+moe_status moe_create(const moe_config* cfg, const uint8_t uid[128], int world, int rank,
+                      void* scratch, size_t scratch_bytes, moe_ctx** out) {
+  if (!out) return fail(MOE_ERR_ARG, "null ctx output");
+  *out = nullptr;
+  Dims d;
+  std::string why;
+  moe_status s = make_dims(cfg, world, rank, &d, &why);
+  if (s != MOE_OK) return fail(s, why);
+  moe_comm* m = nullptr;
+  if (world > 1) {
+    if (!uid) return fail(MOE_ERR_ARG, "uid required when world > 1");
+    s = comm_create(cfg, 1, uid, nullptr, world, rank, &m, &why);
+    if (s != MOE_OK) return fail(s, why);
+    m->private_to_ctx = true;
+  }
+  s = make_ctx(cfg, m, world, rank, scratch, scratch_bytes, out);
+  if (s != MOE_OK && m) {
+    const std::string keep = g_detail;
+    comm_destroy(m);
+    g_detail = keep;
+  }
+  return s;
+}
+
+moe_status moe_create_on_comm(const moe_config* cfg, moe_comm* comm, void* scratch, size_t scratch_bytes,
+                              moe_ctx** out) {
+  if (!out || !comm) return fail(MOE_ERR_ARG, "null comm / ctx output");
+  *out = nullptr;
+  return make_ctx(cfg, comm, comm->plan.world, comm->plan.rank, scratch, scratch_bytes, out);
+}
+
 moe_status moe_destroy(moe_ctx* c) {
   if (!c) return MOE_OK;
-  if (c->d.peer) {
+  moe_comm* m = c->comm;
+  if (m) {
     cudaDeviceSynchronize();
     teardown_peer(c);
+    m->refs -= 1;
+    if (m->private_to_ctx) comm_destroy(m);
   }
-  if (c->tp_comm) ncclCommDestroy(c->tp_comm);
-  if (c->ep_comm) ncclCommDestroy(c->ep_comm);
-  if (c->world_comm) ncclCommDestroy(c->world_comm);
   delete c;
   return MOE_OK;
 }
@@ -860,6 +905,7 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
                        void* y, void* saved, const int32_t* forced_expert, void* stream) {
   if (!c) return fail(MOE_ERR_ARG, "null ctx");
   if (c->poisoned) return fail(MOE_ERR_STATE, "ctx poisoned by an earlier CUDA/NCCL failure");
+  if (c->comm) TRY(check_comm(c));
   if (!x || !wg || !w1 || !w2 || !y || !saved) return fail(MOE_ERR_ARG, "null tensor pointer");
   if (c->d.forced != (forced_expert != nullptr))
     return fail(MOE_ERR_ARG, "forced_expert must be given iff MOE_F_FORCED_ROUTING");
@@ -896,14 +942,16 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
     CUDA_TRY(c, route(ra, st));
   }
 
-  // ring slot of the peer windows used by this forward
-  const int rslot = (int)(c->gen & 1);
-  const uint64_t mygen = ++c->gen;
+  // ring slot of the peer windows used by this forward (the same on every rank: every
+  // rank issues the same sequence of forwards on the communicator)
+  moe_comm* m = c->comm;
+  const int rslot = m ? (int)(m->gen % (uint64_t)m->plan.depth) : 0;
+  const uint64_t mygen = m ? ++m->gen : 0;
   TRY(forward_core(c, x, w1, w2, y, saved, st, 0, rslot));
   if (d.ckpt && c->replayed == saved) c->replayed = nullptr;  // G/A in scratch are stale now
   c->saved_written.insert(saved);
   c->saved_slot[saved] = {rslot, mygen};
-  c->ring_gen[rslot] = mygen;
+  if (m && d.peer) m->ring_gen[rslot] = mygen;
   c->last_saved = saved;
   c->last_stream = st;
   return MOE_OK;
@@ -914,6 +962,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
                         void* dw1, void* dw2, void* stream) {
   if (!c) return fail(MOE_ERR_ARG, "null ctx");
   if (c->poisoned) return fail(MOE_ERR_STATE, "ctx poisoned by an earlier CUDA/NCCL failure");
+  if (c->comm) TRY(check_comm(c));
   if (!dy || !saved || !x || !wg || !w1 || !w2 || !dx || !dwg || !dw1 || !dw2)
     return fail(MOE_ERR_ARG, "null tensor pointer");
   if (!c->saved_written.count(saved))
@@ -923,9 +972,9 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     return fail(MOE_ERR_STATE, "checkpointed forward: call moe_forward_replay on this saved blob first");
   if (c->d.peer && !c->d.ckpt) {
     const auto it = c->saved_slot.find(saved);
-    if (it == c->saved_slot.end() || c->ring_gen[it->second.first] != it->second.second)
-      return fail(MOE_ERR_STATE, "saved blob's peer window was reused: more than 1 newer forward ran "
-                                 "before this backward (ring of 2)");
+    if (it == c->saved_slot.end() || c->comm->ring_gen[it->second.first] != it->second.second)
+      return fail(MOE_ERR_STATE, "saved blob's peer window was reused: ring_depth or more newer forwards "
+                                 "ran on the communicator before this backward");
     rslot = it->second.first;
   }
   if (!aligned16(dy) || !aligned16(x) || !aligned16(wg) || !aligned16(w1) || !aligned16(w2) ||
@@ -944,16 +993,16 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   const float* logits = at<float>(saved, sv.logits);
   const int32_t* count = at<int32_t>(saved, sv.count);
   const bool win_xo = d.peer && !d.ckpt;  // X/O in the ring windows (else saved / CAC stash)
-  const void* X = win_xo ? c->win[moe_ctx::W_X0 + rslot] : at<uint8_t>(saved, sv.X);
+  const void* X = win_xo ? c->comm->win[c->comm->wx(rslot)] : at<uint8_t>(saved, sv.X);
   const void* G = d.ckpt ? at<uint8_t>(c->scratch, sc.Grec) : at<uint8_t>(saved, sv.G);
   const void* A = d.ckpt ? at<uint8_t>(c->scratch, sc.Arec) : at<uint8_t>(saved, sv.A);
-  const void* O = win_xo ? c->win[moe_ctx::W_O0 + rslot] : at<uint8_t>(saved, sv.O);
+  const void* O = win_xo ? c->comm->win[c->comm->wo(rslot)] : at<uint8_t>(saved, sv.O);
   float* dp = at<float>(c->scratch, sc.dp);
-  void* dY = d.peer ? c->win[moe_ctx::W_DY] : at<uint8_t>(c->scratch, sc.dY);
+  void* dY = d.peer ? c->comm->win[moe_comm::W_DY] : at<uint8_t>(c->scratch, sc.dY);
   void* dO = at<uint8_t>(c->scratch, sc.dO);
   void* dH = at<uint8_t>(c->scratch, sc.dH);
-  void* dXp = d.peer && d.Gt > 1 ? c->win[moe_ctx::W_DXP] : at<uint8_t>(c->scratch, sc.dXp);
-  void* dS = d.peer ? c->win[moe_ctx::W_DS] : at<uint8_t>(c->scratch, sc.dS);
+  void* dXp = d.peer && d.Gt > 1 ? c->comm->win[moe_comm::W_DXP] : at<uint8_t>(c->scratch, sc.dXp);
+  void* dS = d.peer ? c->comm->win[moe_comm::W_DS] : at<uint8_t>(c->scratch, sc.dS);
 
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
   const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;  // as in forward_core
@@ -968,14 +1017,14 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[3], 0));
     {
       Scope sx_(c, MOE_K_XFER, c->side, 0);
-      TRY(exchange_ce_dispatch_sig(c, dO, moe_ctx::W_DY, c->side, &sig));
+      TRY(exchange_ce_dispatch_sig(c, dO, moe_comm::W_DY, c->side, &sig));
     }
     ledger(c, MOE_COLL_A2A, 1, c->disp_bytes[1]);
   } else if (d.peer) {
     {
       Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
       CUDA_TRY(c, combine_bwd_peer(dy, O, expert, slot, prob, count, nullptr, ss, d.T, lo, hi, dp,
-                                   peer_dst(c, moe_ctx::W_DY), st));
+                                   peer_dst(c, moe_comm::W_DY), st));
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, 1, st));
@@ -1034,10 +1083,10 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       Scope sc_(c, MOE_K_COMM, st, 0);
       TRY(barrier(c, st));  // every TP partial of dX complete
       ReduceReturn rr;
-      rr.table = c->d_table;
-      rr.nwin = moe_ctx::NWIN;
-      rr.src_win = moe_ctx::W_DXP;
-      rr.dst_win = moe_ctx::W_DS;
+      rr.table = c->comm->d_table;
+      rr.nwin = c->comm->nwin;
+      rr.src_win = moe_comm::W_DXP;
+      rr.dst_win = moe_comm::W_DS;
       rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E;
       rr.H = d.H; rr.Cs = d.Cs; rr.dtd = d.dtd ? 1 : 0;
       CUDA_TRY(c, reduce_return(rr, st));
@@ -1069,7 +1118,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     }
     {
       Scope sx_(c, MOE_K_XFER, c->side, 0);
-      TRY(exchange_ce(c, dXp, moe_ctx::W_DS, 0, d.El, c->side));
+      TRY(exchange_ce(c, dXp, moe_comm::W_DS, 0, d.El, c->side));
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[1], c->side));
     if (c->overlap) {
@@ -1078,7 +1127,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[1], 0));
-    TRY(exchange_local(c, dXp, moe_ctx::W_DS, st));
+    TRY(exchange_local(c, dXp, moe_comm::W_DS, st));
     TRY(barrier(c, st));
     if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
     if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
@@ -1116,6 +1165,7 @@ moe_status moe_forward_replay(moe_ctx* c, const void* saved, const void* x, cons
                               const void* w1, const void* w2, void* stream) {
   if (!c) return fail(MOE_ERR_ARG, "null ctx");
   if (c->poisoned) return fail(MOE_ERR_STATE, "ctx poisoned by an earlier CUDA/NCCL failure");
+  if (c->comm) TRY(check_comm(c));
   if (!c->d.ckpt) return fail(MOE_ERR_STATE, "moe_forward_replay needs MOE_F_CHECKPOINT");
   if (!saved || !x || !wg || !w1 || !w2) return fail(MOE_ERR_ARG, "null tensor pointer");
   if (!c->saved_written.count(saved))
@@ -1134,8 +1184,12 @@ moe_status moe_forward_replay(moe_ctx* c, const void* saved, const void* x, cons
   } else {
     // plain activation checkpointing: the whole forward again (routing record reused:
     // it is deterministic and needs no communication), every collective re-issued
-    const int rslot = (int)(c->gen & 1);
-    ++c->gen;
+    moe_comm* m = c->comm;
+    const int rslot = m ? (int)(m->gen % (uint64_t)m->plan.depth) : 0;
+    if (m) {
+      const uint64_t g = ++m->gen;
+      if (d.peer) m->ring_gen[rslot] = g;
+    }
     TRY(forward_core(c, x, w1, w2, nullptr, sv_mut, st, 2, rslot));
   }
   (void)wg;
@@ -1201,13 +1255,15 @@ moe_status moe_stats_get(moe_ctx* c, moe_stats* out) {
   }
   c->spans.clear();
   c->stats.nccl_async_error = 0;
-  ncclComm_t comms[3] = {c->world_comm, c->tp_comm, c->ep_comm};
+  ncclComm_t comms[3] = {c->comm ? c->comm->world_comm : nullptr, c->comm ? c->comm->tp_comm : nullptr,
+                         c->comm ? c->comm->ep_comm : nullptr};
   for (ncclComm_t m : comms) {
     if (!m) continue;
     ncclResult_t ae = ncclSuccess;
     if (ncclCommGetAsyncError(m, &ae) == ncclSuccess && ae != ncclSuccess) c->stats.nccl_async_error = (int)ae;
   }
   *out = c->stats;
+  if (c->comm) return check_comm(c);
   return MOE_OK;
 }
 

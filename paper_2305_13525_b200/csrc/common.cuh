@@ -172,44 +172,6 @@ __device__ __forceinline__ void ffma2(float2& d, const float2 a, const float2 b)
         "l"(*reinterpret_cast<const unsigned long long*>(&b)));
 }
 
-// ---------------------------------------------------------------- gate weight staging
-// Wg [H][E] fp32 is staged in shared memory per H-chunk of `hch` (multiple of 256)
-// as ws[e][blk][half][lane][4] with h_local = 256 blk + 8 lane + 4 half + q: the
-// two LDS.128 a warp issues per (e, blk) read 512 contiguous bytes each (4
-// wavefronts, no bank conflicts), and lane `lane` receives Wg[h][e] for exactly
-// the 8 h values of its 16-byte x vector.
-__device__ __forceinline__ int ws_index(int e, int hl, int hch) {
-  const int blk = hl >> 8, r = hl & 255, ln = r >> 3, half = (r >> 2) & 1, q = r & 3;
-  return e * hch + blk * 256 + half * 128 + ln * 4 + q;
-}
-
-// Coalesced over the global [H][E] array; entries for h >= H are zero. 16 loads
-// per thread are issued before their shared-memory stores.
-__device__ __forceinline__ void stage_wg(float* ws, const float* __restrict__ wg, int h0, int hch,
-                                         int H, int E) {
-  constexpr int U = 16;
-  const int n = hch * E;
-  const int nt = blockDim.x;
-  const float* src = wg + (size_t)h0 * E;
-  const int valid = (H - h0 < hch ? H - h0 : hch) * E;
-  for (int b = threadIdx.x; b < n; b += U * nt) {
-    float v[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = b + k * nt;
-      v[k] = i < valid ? __ldg(src + i) : 0.f;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = b + k * nt;
-      if (i < n) {
-        const int hl = i / E, e = i - hl * E;
-        ws[ws_index(e, hl, hch)] = v[k];
-      }
-    }
-  }
-}
-
 // Largest multiple of 256 with hch * emax * 4 <= 128 KiB.
 __host__ __device__ constexpr int wg_chunk(int emax) { return (128 * 1024 / (emax * 4)) & ~255; }
 
@@ -273,23 +235,6 @@ __device__ __forceinline__ void tc_commit_2sm(uint32_t bar, uint16_t mask) {
 
 namespace moe {
 
-// ---------------------------------------------------------------- TMA store (bulk groups)
-__device__ __forceinline__ void tma_store_3d(const void* desc, uint32_t src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(desc)),
-               "r"(src), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// Wait until at most 1 committed bulk group still reads shared memory.
-__device__ __forceinline__ void bulk_wait_read_1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-// Make generic-proxy shared-memory writes visible to the async proxy (TMA).
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -355,11 +300,6 @@ __device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
   asm("mul.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
   return u2f(d);
 }
-__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
-  unsigned long long d;
-  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
-  return u2f(d);
-}
 __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
   unsigned long long d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
@@ -398,26 +338,6 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
                : "r"(addr)
                : "memory");
   return r;
-}
-
-// ---------------------------------------------------------------- 1-D bulk copies (TMA engine)
-// global -> shared, completion counted on an mbarrier (bytes % 16 == 0, 16-B aligned)
-__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-// shared -> global, tracked by bulk groups (bulk_commit / wait_group)
-__device__ __forceinline__ void bulk_store_1d(void* dst, uint32_t src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
-               : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void named_bar_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 }  // namespace moe

@@ -6,6 +6,7 @@
 // mantissa bits (relative error ~2^-17 per term, far inside the 1e-2 gradient
 // tolerance); x is exact bf16. Routing-critical arithmetic (the forward gate) stays
 // on fp32 CUDA cores in route.cu.
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -501,7 +502,7 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   auto slice_bytes = [&](int hs) { return (size_t)(((ntiles + hs - 1) / hs + 7) & ~7) * KS * 256; };
   while (slice_bytes(hsplit) > (size_t)budget && hsplit < ntiles / 8) hsplit *= 2;
   const size_t smem = slice_bytes(hsplit);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gate_bwd_dx_mma_kernel<EPK, KC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -22,6 +22,7 @@
 //    dGeLU becomes one multiply and Hpre itself is never stored.
 //  * no split-K: a row's result never depends on its position, which DTD's
 //    bitwise-equality property relies on.
+#include <atomic>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -583,7 +584,7 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 template <int A_MN, int B_MN, int EPI>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
   auto k = gemm_kernel<A_MN, B_MN, EPI>;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -598,7 +599,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
 template <int A_MN, int B_MN, int EPI>
 cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ta2, const CUtensorMap& tb2,
                     const Params& p, cudaStream_t s) {
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
   auto k = gemm2_kernel<A_MN, B_MN, EPI>;
   constexpr int SMEM2_BYTES = smem2_bytes(EPI);
   if (!attr) {

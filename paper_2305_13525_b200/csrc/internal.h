@@ -147,12 +147,13 @@ struct ReduceReturn {
 };
 cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s);
 // (peer.cu) one-sided readiness flag: store `epoch` to flag (a peer's flag slot) after the
-// stream's prior work; wait until *flag >= epoch (wrap-safe).
+// stream's prior work; wait until *flag >= epoch (wrap-safe). Waits are bounded: after
+// timeout_ns the kernel records a code in *err (host-mapped) and returns.
 cudaError_t peer_signal(uint32_t* flag, uint32_t epoch, cudaStream_t s);
-cudaError_t peer_wait(const uint32_t* flag, uint32_t epoch, cudaStream_t s);
+cudaError_t peer_wait(const uint32_t* flag, uint32_t epoch, int32_t* err, uint64_t timeout_ns, cudaStream_t s);
 // Flag barrier over the peer windows (window `win` holds one uint32 slot per rank).
 cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
-                         uint32_t epoch, cudaStream_t s);
+                         uint32_t epoch, int32_t* err, uint64_t timeout_ns, cudaStream_t s);
 
 // Destination of slot-space rows in the expert-space windows of the EP/TP peers
 // (fused dispatch / combine-backward): slot (tt, e, cs) of this rank lands at

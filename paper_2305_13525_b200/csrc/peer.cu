@@ -40,22 +40,46 @@ __global__ void __launch_bounds__(XC_THREADS)
   __threadfence_system();
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded acquire-spin until *flag >= epoch (wrap-safe). Gives up after timeout_ns and
+// records `code` in the host-mapped error word, which the next library call reports
+// (MOE_ERR_TIMEOUT); once the word is set no later wait spins at all, so a dead or
+// absent rank costs one deadline, not one per barrier.
+__device__ __forceinline__ bool bounded_wait(const uint32_t* flag, uint32_t epoch, int32_t* err,
+                                             uint64_t timeout_ns, int32_t code) {
+  if (*reinterpret_cast<volatile int32_t*>(err) != 0) return false;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int32_t)(v - epoch) >= 0) return true;
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicCAS(err, 0, code);
+      __threadfence_system();
+      return false;
+    }
+    __nanosleep(100);
+  }
+}
+
 // Cross-rank barrier over peer memory: thread r stores `epoch` into rank r's flag
-// slot for this rank (release, system scope), then acquire-spins until rank r has
-// stored `epoch` into ours. Launched after the copy kernel it publishes (stream
+// slot for this rank (release, system scope), then acquire-spins (bounded) until rank r
+// has stored `epoch` into ours. Launched after the copy kernel it publishes (stream
 // order), so every write of that kernel precedes the flag.
 __global__ void peer_barrier_kernel(void* const* __restrict__ table, int nwin, int win, int world,
-                                    int rank, uint32_t epoch) {
+                                    int rank, uint32_t epoch, int32_t* err, uint64_t timeout_ns) {
   const int r = threadIdx.x;
   if (r >= world) return;
   uint32_t* remote = static_cast<uint32_t*>(table[(size_t)r * nwin + win]);
   uint32_t* mine = static_cast<uint32_t*>(table[(size_t)rank * nwin + win]);
   __threadfence_system();
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(remote + rank), "r"(epoch) : "memory");
-  uint32_t v;
-  do {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine + r) : "memory");
-  } while ((int32_t)(v - epoch) < 0);
+  bounded_wait(mine + r, epoch, err, timeout_ns, 1);
 }
 
 // Fused TP reduction + return exchange (F8-F10 / B7-B9 for G_t > 1): one warp per
@@ -139,11 +163,8 @@ __global__ void peer_signal_kernel(uint32_t* flag, uint32_t epoch) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
 }
 
-__global__ void peer_wait_kernel(const uint32_t* flag, uint32_t epoch) {
-  uint32_t v;
-  do {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-  } while ((int32_t)(v - epoch) < 0);
+__global__ void peer_wait_kernel(const uint32_t* flag, uint32_t epoch, int32_t* err, uint64_t timeout_ns) {
+  bounded_wait(flag, epoch, err, timeout_ns, 2);
 }
 
 }  // namespace
@@ -153,8 +174,9 @@ cudaError_t peer_signal(uint32_t* flag, uint32_t epoch, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t peer_wait(const uint32_t* flag, uint32_t epoch, cudaStream_t s) {
-  peer_wait_kernel<<<1, 1, 0, s>>>(flag, epoch);
+cudaError_t peer_wait(const uint32_t* flag, uint32_t epoch, int32_t* err, uint64_t timeout_ns,
+                      cudaStream_t s) {
+  peer_wait_kernel<<<1, 1, 0, s>>>(flag, epoch, err, timeout_ns);
   return cudaGetLastError();
 }
 
@@ -166,8 +188,9 @@ cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s) {
 }
 
 cudaError_t peer_barrier(void* const* d_table, int nwin, int win, int world, int rank,
-                         uint32_t epoch, cudaStream_t s) {
-  peer_barrier_kernel<<<1, 32 * ((world + 31) / 32), 0, s>>>(d_table, nwin, win, world, rank, epoch);
+                         uint32_t epoch, int32_t* err, uint64_t timeout_ns, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 32 * ((world + 31) / 32), 0, s>>>(d_table, nwin, win, world, rank, epoch, err,
+                                                              timeout_ns);
   return cudaGetLastError();
 }
 

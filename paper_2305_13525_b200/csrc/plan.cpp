@@ -74,6 +74,15 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->aux_coef = d->aux ? c->aux_loss_coef : 0.f;
   if ((c->flags & MOE_F_CAC) && !d->ckpt) { *why = "MOE_F_CAC needs MOE_F_CHECKPOINT"; return MOE_ERR_ARG; }
   if (d->R > (int64_t)1 << 30) { *why = "rows per expert too large"; return MOE_ERR_SHAPE; }
+  if (c->ring_depth < 0 || c->ring_depth > 64) { *why = "ring_depth must be in [0, 64]"; return MOE_ERR_ARG; }
+  if (c->peer_timeout_ms < 0) { *why = "peer_timeout_ms must be >= 0"; return MOE_ERR_ARG; }
+  d->ring_depth = c->ring_depth ? c->ring_depth : 2;
+  d->timeout_ms = c->peer_timeout_ms ? c->peer_timeout_ms : 60000;
+  if (d->peer && d->dtd && d->Gt > 8) {
+    // the fused peer dispatch / combine-backward resolve at most 8 destination rows per slot
+    *why = "the peer-memory exchange supports DTD with g_tensor <= 8 (use MOE_F_NCCL_EXCHANGE)";
+    return MOE_ERR_UNSUPPORTED;
+  }
   return MOE_OK;
 }
 

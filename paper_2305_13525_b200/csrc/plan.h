@@ -29,6 +29,8 @@ struct Dims {
   bool aux;          // MOE_F_AUX_LOSS
   float aux_coef;
   int K;             // experts per token (top_k: 1 or 2)
+  int ring_depth;    // forwards in flight per communicator (peer windows of X, O)
+  int64_t timeout_ms;  // deadline of a peer barrier / signal wait
 };
 
 // Validates and derives; returns MOE_OK or an error with *why set.

@@ -13,6 +13,7 @@
 // 1024-token blocks: (a) per-block warp-match ranks + block histogram,
 // (b) block prefix per expert, slot/keep decision, count[E], and the inverse
 // map tok_of[e][slot] used by the slot-parallel dispatch.
+#include <atomic>
 #include <float.h>
 
 #include "common.cuh"
@@ -438,7 +439,7 @@ __global__ void aux_final_kernel(const float* __restrict__ partial, int64_t T, i
   }
 }
 
-int g_sms = 0;
+std::atomic<int> g_sms{0};
 
 template <int EMAX, int TPW, int WARPS>
 cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
@@ -446,7 +447,7 @@ cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
   const int hpad = (a.H + 255) & ~255;
   const int hch = hpad < hmax ? hpad : hmax;
   const int smem = EMAX * hch * 4 + WARPS * 2 * TPW * 256 * 2;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gate_kernel<EMAX, TPW, WARPS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -455,9 +456,10 @@ cudaError_t launch_gate(const RouteArgs& a, cudaStream_t s) {
     attr = true;
   }
   if (!g_sms) {
-    int dev = 0;
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms = n;
   }
   const int64_t per_cta = (int64_t)WARPS * TPW;
   int64_t grid = (a.T + per_cta - 1) / per_cta;
@@ -478,7 +480,7 @@ template <int EG>
 cudaError_t launch_gate_split(const RouteArgs& a, int hpad, cudaStream_t s) {
   constexpr int TPW = 4, WARPS = 16;
   const int smem = EG * hpad * 4 + WARPS * 2 * TPW * 256 * 2;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gate_kernel<EG, TPW, WARPS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,9 +489,10 @@ cudaError_t launch_gate_split(const RouteArgs& a, int hpad, cudaStream_t s) {
     attr = true;
   }
   if (!g_sms) {
-    int dev = 0;
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms = n;
   }
   const int groups = (a.E + EG - 1) / EG;
   const int64_t per_cta = (int64_t)WARPS * TPW;

@@ -53,3 +53,35 @@ def routing_protocol(gpu_expert, gpu_gap, r: O.Routing):
     assert bad.size == 0, f"routing mismatch outside tie set at tokens {bad[:10]}"
     idx = np.nonzero(tie)[0]
     return idx, ge[idx]
+
+
+ROW_REL_BAR = 5e-2  # per-row bound beside the global one: a single corrupted row cannot hide
+
+
+def row_errors(got, ref, axis_rows: int = -1):
+    """Per-row relative L2 of got vs ref (rows = all but the last axis). Rows whose
+    reference is exactly zero (dropped tokens, experts with no tokens) must be exactly
+    zero on the GPU too; returns (max rel over nonzero rows, #zero rows violated)."""
+    g = np.asarray(got, dtype=np.float64).reshape(-1, np.asarray(got).shape[-1])
+    r = np.asarray(ref, dtype=np.float64).reshape(-1, np.asarray(ref).shape[-1])
+    nr = np.linalg.norm(r, axis=1)
+    nd = np.linalg.norm(g - r, axis=1)
+    nz = nr > 0
+    worst = float((nd[nz] / nr[nz]).max()) if nz.any() else 0.0
+    bad_zero = int(np.count_nonzero(nd[~nz] > 0))
+    return worst, bad_zero
+
+
+def parity_failures(name: str, got, ref, rows: bool = True) -> list[str]:
+    """Global rel L2 <= 1e-2 (BASELINE.json) and, per row, <= 5e-2 with exact zeros."""
+    out = []
+    e = rel_l2(got, ref)
+    if not e <= REL_L2_BAR:
+        out.append(f"{name}: rel L2 {e:.3e} > {REL_L2_BAR}")
+    if rows and np.asarray(ref).ndim >= 2:
+        worst, bad_zero = row_errors(got, ref)
+        if not worst <= ROW_REL_BAR:
+            out.append(f"{name}: worst row rel L2 {worst:.3e} > {ROW_REL_BAR}")
+        if bad_zero:
+            out.append(f"{name}: {bad_zero} rows nonzero where the oracle is exactly zero")
+    return out

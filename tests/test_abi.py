@@ -39,9 +39,9 @@ def test_library_exports_every_header_symbol():
 
 def test_status_strings():
     L = binding.lib()
-    names = [L.moe_status_string(i).decode() for i in range(8)]
+    names = [L.moe_status_string(i).decode() for i in range(9)]
     assert names == ["MOE_OK", "MOE_ERR_ARG", "MOE_ERR_SHAPE", "MOE_ERR_ALIGN", "MOE_ERR_STATE",
-                     "MOE_ERR_CUDA", "MOE_ERR_NCCL", "MOE_ERR_UNSUPPORTED"]
+                     "MOE_ERR_CUDA", "MOE_ERR_NCCL", "MOE_ERR_UNSUPPORTED", "MOE_ERR_TIMEOUT"]
 
 
 @pytest.mark.parametrize("kw,status", [
@@ -206,3 +206,79 @@ def test_checkpoint_saved_blob_drops_activations():
     assert s0 - s1 == 2 * ffn           # G and A are re-materialized by the replay
     with pytest.raises(MoEError):       # CAC without checkpointing is rejected
         moe_plan_bytes(MoEConfig(base.tokens, base.hidden, base.ffn, base.experts, flags=1 | MOE_F_CAC))
+
+
+# ---------------------------------------------------------------- shared communicator (host plan)
+def _mib2(b):
+    return (b + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+
+
+def test_comm_plan_bytes_window_formula():
+    """Window memory of a communicator (include/moe.h moe_comm_plan_bytes): a ring of
+    ring_depth (X, O) window pairs + dY, dS (+ the two TP-partial windows when G_t > 1) +
+    the flag page and metadata, each rounded to the 2 MiB allocation granularity."""
+    from paper_2305_13525_b200 import moe_comm_plan_bytes
+    cfg = MoEConfig.from_shape(synth.CONFIGS["6.7b-tp2ep4"])
+    L = moe_plan_layout(cfg, 8, 0)
+    xe = L["experts_local"] * L["rows_per_expert"] * 4096 * 2      # expert space [E_l][R][H]
+    so = 16 * L["capacity"] * 4096 * 2                               # slot space [E][C][H]
+    d2 = moe_comm_plan_bytes([cfg], 8, 0)
+    d3 = moe_comm_plan_bytes([cfg.replace(ring_depth=3)], 8, 0)
+    assert d3 - d2 == _mib2(xe) + _mib2(so)                          # one more ring slot
+    fixed = d2 - 3 * _mib2(xe) - 3 * _mib2(so) - 2 * _mib2(xe)      # X,O ring + dY, dS + Y, dXp
+    assert 0 < fixed <= 2 * (2 << 20)                                # flags + metadata
+    # G_t = 1: no TP-partial windows
+    ep = MoEConfig.from_shape(synth.CONFIGS["2.7b-ep8"])
+    L = moe_plan_layout(ep, 8, 0)
+    xe = L["experts_local"] * L["rows_per_expert"] * 2560 * 2
+    so = 32 * L["capacity"] * 2560 * 2
+    assert moe_comm_plan_bytes([ep], 8, 0) - 3 * _mib2(xe) - 3 * _mib2(so) <= 2 * (2 << 20)
+
+
+def test_comm_plan_shared_by_layers_does_not_scale_with_layer_count():
+    from paper_2305_13525_b200 import moe_comm_plan_bytes
+    cfg = MoEConfig.from_shape(synth.CONFIGS["6.7b-tp2ep4"])
+    one = moe_comm_plan_bytes([cfg], 8, 3)
+    assert moe_comm_plan_bytes([cfg] * 24, 8, 3) == one
+    small = cfg.replace(hidden=1024, ffn=4096)
+    assert moe_comm_plan_bytes([cfg, small], 8, 3) == one            # sized for the largest
+    assert moe_comm_plan_bytes([small], 8, 3) < one
+
+
+def test_comm_plan_no_windows_without_peer_exchange():
+    from paper_2305_13525_b200 import MOE_F_NCCL_EXCHANGE, moe_comm_plan_bytes
+    cfg = MoEConfig.from_shape(synth.CONFIGS["6.7b-tp2ep4"])
+    assert moe_comm_plan_bytes([cfg.replace(flags=cfg.flags | MOE_F_NCCL_EXCHANGE)], 8, 0) == 0
+    assert moe_comm_plan_bytes([MoEConfig.from_shape(synth.CONFIGS["1.3b"])], 1, 0) == 0
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(ring_depth=-1), "MOE_ERR_ARG"),
+    (dict(ring_depth=65), "MOE_ERR_ARG"),
+    (dict(peer_timeout_ms=-5), "MOE_ERR_ARG"),
+])
+def test_comm_config_validation(kw, status):
+    cfg = MoEConfig(4096, 256, 512, 8, 1.0, 2, 2, True, **kw)
+    with pytest.raises(MoEError) as ei:
+        moe_plan_layout(cfg, 4, 0)
+    assert ei.value.name == status
+
+
+def test_comm_plan_rejects_mixed_layouts():
+    from paper_2305_13525_b200 import moe_comm_plan_bytes
+    a = MoEConfig(4096, 256, 512, 8, 1.0, 2, 2, True)
+    with pytest.raises(MoEError) as ei:
+        moe_comm_plan_bytes([a, a.replace(g_tensor=1, g_expert=4)], 4, 0)
+    assert ei.value.name == "MOE_ERR_ARG"
+
+
+def test_peer_dtd_beyond_eight_tp_ranks_is_unsupported():
+    """The fused peer dispatch resolves at most 8 destination rows per slot (G_t <= 8);
+    larger DTD groups must use the NCCL exchange instead of silently dropping rows."""
+    from paper_2305_13525_b200 import MOE_F_NCCL_EXCHANGE
+    cfg = MoEConfig(4096, 256, 16 * 64, 16, 1.0, 16, 1, True)
+    with pytest.raises(MoEError) as ei:
+        moe_plan_layout(cfg, 16, 0)
+    assert ei.value.name == "MOE_ERR_UNSUPPORTED"
+    moe_plan_layout(cfg.replace(flags=cfg.flags | MOE_F_NCCL_EXCHANGE), 16, 0)
+    moe_plan_layout(cfg.replace(dtd=False), 16, 0)
