@@ -35,7 +35,7 @@ __all__ = [
     "decode_bf16", "capacity", "gelu_tanh", "gelu_tanh_grad", "gate", "assign_slots",
     "priority_order", "aux_loss", "aux_loss_dlogits",
     "Routing", "route", "forward_group", "backward_group", "layer",
-    "token_forward", "token_backward", "expert_row_grads", "TIE_GAP",
+    "token_forward", "token_backward", "tokens_forward_backward", "expert_row_grads", "TIE_GAP",
 ]
 
 # BASELINE.json north_star: routing must match bit-exactly "except for logged
@@ -367,3 +367,32 @@ def expert_row_grads(e: int, f: int, xs, dys, w1, w2, routings):
         g1 += dhf @ x[idx]
         g2 += do.T @ af
     return g1, g2
+
+
+def tokens_forward_backward(idx, x, dy, wg, w1, w2, r: Routing):
+    """y_t and dx_t for the tokens `idx` of one group (same definitions as
+    forward_group / backward_group, evaluated only for these tokens, one expert at a
+    time: h = x_t W1_e^T, a = gelu(h), o = a W2_e^T, y_t = p_t o; dx_t = dh W1_e +
+    sum_j dl_tj Wg[:, j] with dl_tj = dp_t p_t (delta_{j,e*} - s_tj); 0 if dropped).
+    Returns (y [n, H], dx [n, H])."""
+    idx = np.asarray(idx, dtype=np.int64)
+    H, E = x.shape[1], wg.shape[1]
+    y = np.zeros((idx.size, H))
+    dx = np.zeros((idx.size, H))
+    for e in range(E):
+        sel = np.nonzero((r.expert[idx] == e) & r.kept[idx])[0]
+        if sel.size == 0:
+            continue
+        t = idx[sel]
+        h = x[t] @ w1[e].T
+        o = gelu_tanh(h) @ w2[e].T
+        y[sel] = r.p[t, None] * o
+        if dy is None:
+            continue
+        dp = np.sum(dy[t] * o, axis=1)
+        dh = ((r.p[t, None] * dy[t]) @ w2[e]) * gelu_tanh_grad(h)
+        onehot = np.zeros((t.size, E))
+        onehot[:, e] = 1.0
+        dl = (dp * r.p[t])[:, None] * (onehot - r.s[t])
+        dx[sel] = dh @ w1[e] + dl @ wg.T
+    return y, dx

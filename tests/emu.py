@@ -230,3 +230,65 @@ def close_failures(res: list[dict], a: str, b: str, bar: float = REL_L2_BAR) -> 
             if not e <= bar:
                 out.append(f"rank {r}: {a} vs {b} rel L2 {e:.3e} for {n}")
     return out
+
+
+def sampled_failures(wl: Workload, res: list[dict], key: str, seed: int = 0) -> tuple[list[str], dict]:
+    """Full-size parity (top-1) without the full oracle layer: routing of every token
+    (tie protocol), slots and counts bit-exact on every rank; y / dx on stratified tokens
+    (one per (expert, 256-row M-tile) of the GEMM rows, plus dropped ones); dW1 rows / dW2
+    columns on one f per 256-wide tile of every local expert of every rank. Each bound:
+    rel L2 <= 1e-2 over the samples and <= 5e-2 per sampled row, exact zeros where the
+    oracle is zero. (dWg needs dp of every token and is checked at reduced sizes.)"""
+    from tests.helpers import LazyExperts, stratified_f, stratified_tokens
+    fails, errs = [], {}
+    wg = wl.wg.astype(np.float64)
+    E = wg.shape[1]
+    cap = O.capacity(wl.T, E, wl.shape.cf, wl.gt)
+    w1, w2 = LazyExperts(wl.w1), LazyExperts(wl.w2)
+    for d in range(wl.gd):
+        groups = [d * wl.gep + ep for ep in range(wl.gep)]
+        xs = [O.decode_bf16(wl.xs[s]) for s in groups]
+        dys = [O.decode_bf16(wl.dys[s]) for s in groups]
+        routings = []
+        for ep, s in enumerate(groups):
+            g = res[(d * wl.gep + ep) * wl.gt][key]["rt"]
+            r0 = O.route(xs[ep], wg, cap)
+            tie = (r0.gap < O.TIE_GAP) | (g["gap"] < O.TIE_GAP)
+            bad = np.nonzero((g["expert"] != r0.expert) & ~tie)[0]
+            if bad.size:
+                fails.append(f"{key} group {s}: routing mismatch outside ties at {bad[:8]}")
+            routings.append(O.route(xs[ep], wg, cap, override=(np.nonzero(tie)[0], g["expert"][tie])))
+        for ep, r in enumerate(routings):
+            for t in range(wl.gt):
+                g = res[(d * wl.gep + ep) * wl.gt + t][key]
+                if not np.array_equal(g["rt"]["slot"], r.slot) or not np.array_equal(g["rt"]["count"], r.count):
+                    fails.append(f"{key} rank {(d * wl.gep + ep) * wl.gt + t}: slots/counts differ")
+            toks = stratified_tokens(r, ep, seed=seed)
+            yr, dxr = O.tokens_forward_backward(toks, xs[ep], dys[ep], wg, w1, w2, r)
+            g = res[(d * wl.gep + ep) * wl.gt][key]
+            for name, got, want in (("y", g["y"], yr), ("dx", g["dx"], dxr)):
+                gv = tensor_f64(got[torch.from_numpy(toks).to(got.device)])
+                errs[(d, ep, name)] = rel_l2(gv, want)
+                fails += [f"{key} group {groups[ep]} {m}" for m in parity_failures(name, gv, want)]
+        for ep in range(wl.gep):
+            for t in range(wl.gt):
+                rank = (d * wl.gep + ep) * wl.gt + t
+                g = res[rank][key]
+                El, Fl = g["layout"]["experts_local"], g["layout"]["ffn_local"]
+                fl = stratified_f(Fl, seed=seed + rank)
+                got1, want1, got2, want2 = [], [], [], []
+                d1, d2 = g["dw1"], g["dw2"]
+                for el in range(El):
+                    e = ep * El + el
+                    for f in fl:
+                        a, b = O.expert_row_grads(e, t * Fl + int(f), xs, dys, w1, w2, routings)
+                        want1.append(a)
+                        want2.append(b)
+                    fi = torch.from_numpy(fl).to(d1.device)
+                    got1.append(tensor_f64(d1[el].index_select(0, fi)))
+                    got2.append(tensor_f64(d2[el].index_select(1, fi).t()))
+                for name, got, want in (("dw1", np.concatenate(got1), np.array(want1)),
+                                        ("dw2", np.concatenate(got2), np.array(want2))):
+                    errs[(rank, name)] = rel_l2(got, want)
+                    fails += [f"{key} rank {rank} {m}" for m in parity_failures(name, got, want)]
+    return fails, errs

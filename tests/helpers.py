@@ -85,3 +85,44 @@ def parity_failures(name: str, got, ref, rows: bool = True) -> list[str]:
         if bad_zero:
             out.append(f"{name}: {bad_zero} rows nonzero where the oracle is exactly zero")
     return out
+
+
+class LazyExperts:
+    """Expert weights decoded to float64 one expert at a time (full-size shapes do not fit
+    as a float64 [E, F, H] array); indexable like the stacked array: w[e] -> [F, H]."""
+
+    def __init__(self, bits):
+        self.bits = bits
+        self._e, self._v = None, None
+
+    def __getitem__(self, e):
+        e = int(e)
+        if e != self._e:
+            self._e, self._v = e, O.decode_bf16(self.bits[e])
+        return self._v
+
+
+def stratified_tokens(r: "O.Routing", src_block: int, tile: int = 256, seed: int = 0, extra: int = 4):
+    """One kept token per (expert, `tile`-row M-tile) of the expert GEMMs — a token of
+    source block s with slot c is row s*C + c of its expert's [G_ep*C] rows — plus a few
+    dropped tokens and the first / last token. Covers every M-tile of every expert."""
+    rng = np.random.default_rng(seed)
+    picks = [0, len(r.expert) - 1]
+    for e in range(len(r.count)):
+        kept = np.nonzero((r.expert == e) & r.kept)[0]
+        if kept.size == 0:
+            continue
+        tiles = (src_block * r.cap + r.slot[kept]) // tile
+        for tl in np.unique(tiles):
+            picks.append(int(rng.choice(kept[tiles == tl])))
+    dropped = np.nonzero(~r.kept)[0]
+    if dropped.size:
+        picks += [int(t) for t in rng.choice(dropped, min(extra, dropped.size), replace=False)]
+    return np.array(sorted(set(picks)), dtype=np.int64)
+
+
+def stratified_f(F_local: int, tile: int = 256, seed: int = 0):
+    """One index per `tile`-wide block of [0, F_local): covers every dW1 M-tile (rows f)
+    and every dW2 N-tile (columns f) of the weight-gradient GEMMs."""
+    rng = np.random.default_rng(seed)
+    return np.array([min(b + int(rng.integers(tile)), F_local - 1) for b in range(0, F_local, tile)])

@@ -231,3 +231,27 @@ def test_emulated_absent_rank_times_out():
 
     res = emu.run_modes(wl, {"k": cfg}, schedule=sched)
     assert res[0]["k"]["names"] == ["MOE_ERR_TIMEOUT", "MOE_ERR_STATE"], res[0]
+
+
+# ---------------------------------------------------------------- BASELINE shapes, 8 emulated ranks
+@pytest.mark.parametrize("name,T", [("2.7b-ep8", 2048), ("6.7b-tp2ep4", 2048),
+                                    ("2.7b-ep8", 16384), ("6.7b-tp2ep4", 16384)])
+def test_emulated_baseline_shapes_sampled(name, T):
+    """BASELINE configs[2] (2.7B, E 32, EP over 8) and configs[3] (6.7B, E 16, G_t = 2 x
+    G_ep = 4, DTD vs vanilla) with all 8 ranks emulated, at T = 2048 per group and at the
+    full T = 16384 the bench times: routing of every token bit-exact, y / dx on one token
+    per (expert, 256-row M-tile), dW1 / dW2 on one f per 256-wide tile of every local
+    expert of every rank (tests/emu.py sampled_failures)."""
+    shape = synth.CONFIGS[name]
+    wl = emu.Workload(shape, tokens=T)
+    modes = {"dtd": wl.config(True)}
+    if shape.g_tensor > 1:
+        modes["van"] = wl.config(False)
+    res = emu.run_modes(wl, modes)
+    fails, errs = emu.sampled_failures(wl, res, "dtd")
+    if "van" in modes:
+        fails += emu.bitwise_failures(res, "dtd", "van")
+        a2a = [(rr["dtd"]["stats"]["wire_bytes"]["a2a"], rr["van"]["stats"]["wire_bytes"]["a2a"]) for rr in res]
+        fails += [f"a2a {d} x 2 != {v}" for d, v in a2a if d * 2 != v]
+    assert not fails, "\n".join(fails[:40])
+    print(name, T, "max rel L2", {k: max(v for kk, v in errs.items() if kk[-1] == k) for k in ("y", "dx", "dw1", "dw2")})

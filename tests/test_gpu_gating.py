@@ -50,6 +50,12 @@ def check(inp, g, cf, seed=None, coef=0.0):
             "dw2": rel_l2(g["dw2"], ref["dw2"])}
     for k, v in errs.items():
         assert v <= REL_L2_BAR, (k, errs)
+    from tests.helpers import parity_failures
+    rows = []
+    for k in ("y", "dx", "dw1", "dw2"):
+        want = ref[k][0] if k in ("y", "dx") else ref[k]
+        rows += parity_failures(k, g[k], want)
+    assert not rows, rows
     if coef:
         assert g["aux"] == pytest.approx(ref["aux"][0], rel=1e-5)
     return r, ref

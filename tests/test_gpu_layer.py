@@ -58,6 +58,11 @@ def check_parity(inp: Inputs, g, cf, forced=None):
             "dw2": rel_l2(g["dw2"], ref["dw2"])}
     for k, v in errs.items():
         assert v <= REL_L2_BAR, (k, errs)
+    from tests.helpers import parity_failures
+    fails = []
+    for k, want in (("y", ref["y"][0]), ("dx", ref["dx"][0]), ("dw1", ref["dw1"]), ("dw2", ref["dw2"])):
+        fails += parity_failures(k, g[k], want)
+    assert not fails, fails
     # dropped tokens are exact zeros
     assert (g["y"][~r.kept] == 0).all() and (g["dx"][~r.kept] == 0).all()
     return errs
@@ -125,35 +130,42 @@ def test_13b_reduced_tokens_full_parity():
 
 
 def test_13b_full_size_sampled():
-    """BASELINE configs[1] at full size (T = 16384) in the bench's launch
-    configuration: routing bit-exact for all tokens; y/dx on sampled tokens;
-    dW1 rows / dW2 columns on sampled (expert, f)."""
+    """BASELINE configs[1] at full size (T = 16384) in the bench's launch configuration:
+    routing of every token bit-exact; y / dx on one token per (expert, 256-row M-tile) of the
+    expert GEMMs (every M-tile of F6/F7/B4/B5 covered) plus dropped tokens; dW1 rows / dW2
+    columns on one f per 256-wide tile of every expert (every M-tile of dW1 and N-tile of
+    dW2, all H). Global rel L2 <= 1e-2 and <= 5e-2 per sampled row (a single corrupted tile
+    cannot hide under the global norm)."""
+    from tests.helpers import LazyExperts, parity_failures, stratified_f, stratified_tokens
     shape = synth.CONFIGS["1.3b"]
     inp = Inputs(shape)
     g, _ = run_gpu(inp, shape)
-    xs, dys, wg, w1, w2 = inp.oracle_arrays()
+    x = O.decode_bf16(inp.x[0])
+    dy = O.decode_bf16(inp.dy[0])
+    wg = inp.wg.astype(np.float64)
+    w1, w2 = LazyExperts(inp.w1), LazyExperts(inp.w2)
     cap = O.capacity(inp.T, shape.experts, 1.0)
-    r0 = O.route(xs[0], wg, cap)
+    r0 = O.route(x, wg, cap)
     idx, ex = routing_protocol(g["expert"], g["gap"], r0)
-    r = O.route(xs[0], wg, cap, override=(idx, ex))
+    r = O.route(x, wg, cap, override=(idx, ex))
     np.testing.assert_array_equal(g["slot"], r.slot)
     np.testing.assert_array_equal(g["count"], r.count)
-    rng = np.random.default_rng(0)
-    toks = np.concatenate([rng.choice(inp.T, 48, replace=False), np.nonzero(~r.kept)[0][:4], [0, inp.T - 1]])
-    ys, yr, dxs, dxr = [], [], [], []
-    for t in toks:
-        yt, _ = O.token_forward(int(t), xs[0], w1, w2, r)
-        ys.append(g["y"][t]); yr.append(yt)
-        dxs.append(g["dx"][t]); dxr.append(O.token_backward(int(t), xs[0], dys[0], wg, w1, w2, r))
-    assert rel_l2(ys, yr) <= REL_L2_BAR
-    assert rel_l2(dxs, dxr) <= REL_L2_BAR
-    g1s, g1r, g2s, g2r = [], [], [], []
-    for e, f in [(0, 0), (3, 8191), (7, 1234), (15, 4096), (11, 77)]:
-        a, b = O.expert_row_grads(e, f, xs, dys, w1, w2, [r])
-        g1s.append(g["dw1"][e, f]); g1r.append(a)
-        g2s.append(g["dw2"][e, :, f]); g2r.append(b)
-    assert rel_l2(g1s, g1r) <= REL_L2_BAR
-    assert rel_l2(g2s, g2r) <= REL_L2_BAR
+    toks = stratified_tokens(r, 0)
+    assert len(toks) >= shape.experts * (cap // 256)
+    yr, dxr = O.tokens_forward_backward(toks, x, dy, wg, w1, w2, r)
+    fails = parity_failures("y", g["y"][toks], yr) + parity_failures("dx", g["dx"][toks], dxr)
+    fl = stratified_f(shape.ffn)
+    got1, want1, got2, want2 = [], [], [], []
+    for e in range(shape.experts):
+        for f in fl:
+            a, b = O.expert_row_grads(e, int(f), [x], [dy], w1, w2, [r])
+            want1.append(a)
+            want2.append(b)
+            got1.append(g["dw1"][e, f])
+            got2.append(g["dw2"][e, :, f])
+    fails += parity_failures("dw1", np.array(got1), np.array(want1))
+    fails += parity_failures("dw2", np.array(got2), np.array(want2))
+    assert not fails, fails
 
 
 def test_determinism_bitwise():
@@ -207,11 +219,21 @@ def test_checkpoint_replay_bitwise(cac):
             assert ei.value.name == "MOE_ERR_STATE"
             layer.moe_forward_replay(saved, x, wg, w1, w2)
         g = layer.moe_backward(dy, saved, x, wg, w1, w2)
+        rt = layer.moe_routing(saved)
         torch.cuda.synchronize()
         outs.append((y.clone(), *[t.clone() for t in g]))
+        st = layer.moe_stats()
         layer.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+    # the checkpointed path itself against the oracle (the replay must
+    # reproduce the forward's activations, not merely agree with another GPU run)
+    names = ("y", "dx", "dwg", "dw1", "dw2")
+    gck = {k: (tensor_f64(v) if v.dtype == torch.bfloat16 else v.cpu().numpy().astype(np.float64))
+           for k, v in zip(names, outs[1])}
+    gck.update({k: v.cpu().numpy() for k, v in rt.items()})
+    gck["stats"] = st
+    check_parity(inp, gck, 1.0)
 
 
 def test_fused_gate_dx_matches_separate_kernel(monkeypatch):

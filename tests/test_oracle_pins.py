@@ -288,3 +288,17 @@ def test_bf16_decode_exact():
     bits = synth.f32_to_bf16_bits(vals)
     ref = torch.tensor(vals).to(torch.bfloat16).to(torch.float64).numpy()
     np.testing.assert_array_equal(O.decode_bf16(bits), ref)
+
+
+def test_tokens_forward_backward_matches_full_layer():
+    """The subset evaluation used by the full-size sampled parity equals the full layer on
+    every token it is asked for (kept and dropped), in any order, with repeats."""
+    x, wg, w1, w2, dy = _tiny(T=40, H=8, F=6, E=4, seed=13)
+    r = O.route(x, wg, cap=7)
+    y, cache = O.forward_group(x, wg, w1, w2, r)
+    dx, *_ = O.backward_group(x, dy, wg, w1, w2, r, cache)
+    assert (~r.kept).any()
+    idx = np.array([39, 0, 5, 5, 17, *np.nonzero(~r.kept)[0][:3]])
+    ys, dxs = O.tokens_forward_backward(idx, x, dy, wg, w1, w2, r)
+    np.testing.assert_allclose(ys, y[idx], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(dxs, dx[idx], rtol=1e-10, atol=1e-12)
