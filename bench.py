@@ -310,13 +310,18 @@ def main():
     time.sleep(0.3)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
+        marks[i].record(stream)
         step()
+    marks[args.steps].record(stream)
     e1.record(stream)
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+    ms_median = float(np.median(step_ms))
     st = layer.moe_stats()
     ms_t = torch.tensor([ms], device=dev)
     if dist is not None:
@@ -339,10 +344,9 @@ def main():
     gemm_ms = st["kernel_ms"]["gemm"] / args.steps
     peaks, peak_src = load_peaks()
     achieved = gemm_flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
-    # clocks at max during the timed region -> compare with the burst peak (conservative);
-    # power-capped clocks -> the sustained peak (MEASURED_PEAKS.json, B200_PROFILING.md)
-    capped = bool(clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] < 0.97 * clk["sm_max_mhz"])
-    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) if capped else peaks["bf16_tflops"]
+    # frac against the measured burst peak (conservative, the same in every line); the
+    # sustained figure (the GEMMs run inside a long step) is reported beside it
+    peak = peaks["bf16_tflops"]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
@@ -355,7 +359,8 @@ def main():
     gemm_launch_ms = gemm_ms / 6.0
     roofline = {"bound": "tensor", "kernel": "gemm2_kernel (tcgen05 cta_group::2, 6 launches/step)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "peak_kind": f"{peak_src} bf16 {'sustained' if capped else 'burst'}",
+                "peak_kind": f"{peak_src} bf16 burst",
+                "peak_sustained": peaks.get("bf16_tflops_sustained"),
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "frac_of_sustained": (achieved / peaks.get('bf16_tflops_sustained', peak)) if achieved else None,
                 "algorithmic_flop_per_launch": gemm_flops_step / 6.0,
@@ -371,13 +376,16 @@ def main():
     slot_rows = E * C // (gt if (dtd and gt > 1) else 1)
     kept_group = kept_local
     row = H * 2
-    hbm_bytes = {"dispatch": 2 * slot_rows * row,                       # read x row, write slot row
+    hbm_bytes = {"route": T * row + T * E * 4,                          # F1+F2: read x, write logits
+                 "dispatch": 2 * slot_rows * row,                       # read x row, write slot row
                  "combine": 2 * T * row,                                # read O row, write y row
                  "combine_bwd": 2 * T * row + slot_rows * row}          # read dy + O, write dO
     if world == 1:
-        # one GPU: F11 is fused into F7's epilogue (the combine class is only the zeroing of
-        # dropped rows), so it has no separate HBM figure
+        # one GPU: F11 is fused into F7's epilogue (dropped rows are zeroed by the dispatch
+        # launch), so it has no separate HBM figure; the combine-backward launch also
+        # writes dl [T][E] fp32 and the K-extension rows [E*C][64] bf16
         hbm_bytes.pop("combine")
+        hbm_bytes["combine_bwd"] += T * E * 4 * 2 + slot_rows * 128
     hbm = {}
     for k, b in hbm_bytes.items():
         t_ms = per_class.get(k, 0.0)
@@ -385,7 +393,16 @@ def main():
             gbs = b / (t_ms / 1e3) / 1e9
             hbm[k] = {"bytes": b, "ms": t_ms, "GB/s": gbs, "frac": gbs / peaks["hbm_gbs"]}
     if world == 1:
-        hbm["combine"] = "fused into the F7 GEMM epilogue (EPI_COMBINE); class time = zeroing dropped rows"
+        hbm["combine"] = "fused into the F7 GEMM epilogue (EPI_COMBINE); dropped rows zeroed by the dispatch launch"
+    if "route" in hbm:
+        # the gate also has a compute roofline: 2*H*E flop per token (x . Wg); on the tensor
+        # cores with Wg split in three bf16 terms (3x the flops) it is far from that bound,
+        # so HBM (streaming x) is the roofline that binds; the FP32-ALU figure is what the
+        # contraction would need on CUDA cores
+        r_ms = hbm["route"]["ms"]
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s: SMs x FP32 lanes x FMA x max clock
+        hbm["route"]["flop"] = 2.0 * T * H * E
+        hbm["route"]["fp32_alu_frac"] = (2.0 * T * H * E / (r_ms / 1e3) / 1e12) / fp32_peak
     del kept_group
 
     # ---- e2e through the public API with host buffers (pinned). Every step copies its
@@ -468,6 +485,7 @@ def main():
         out = {"metric": "MoE-layer fwd+bwd tokens/s", "value": value, "unit": "tokens/s",
                "value_per_gpu": value / world,
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+               "ms_per_step_median": ms_median,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                "data": "synthetic (x, dy ~ N(0,1); Wg ~ N(0,1/H); W1 ~ N(0,1/H); W2 ~ N(0,1/F))",
                "config": {"workload": name, "tokens_per_group": T, "hidden": H, "ffn": F, "experts": E,

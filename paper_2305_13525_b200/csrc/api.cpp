@@ -530,7 +530,9 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   // overlapped with GEMM1 on the local source block
   const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;
   uint32_t sig = 0;
-  bool fused_combine = false;
+  // One GPU, top-1: F11 fused into F7's epilogue (O still stored for the backward); the
+  // dispatch launch zeroes the y rows of dropped tokens
+  const bool fused_combine = solo && d.K == 1 && y && !c->no_fused_combine;
   if (split) {
     SplitDst sd{X, D, d.ep, d.El, d.Gep};
     {
@@ -554,7 +556,8 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     TRY(publish(c, true, pass, st));
   } else {
     Scope sc_(c, MOE_K_DISPATCH, st, 1);
-    CUDA_TRY(c, dispatch(x, tok_of, count, ss, lo, hi, D, st));
+    CUDA_TRY(c, dispatch(x, tok_of, count, ss, lo, hi, D, at<int32_t>(saved, sv.slot), d.T,
+                         fused_combine ? y : nullptr, st));
   }
   if (!solo && !d.peer) {
     Scope sc_(c, MOE_K_COMM, st, 0);
@@ -640,8 +643,6 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     }
   } else {
     GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
-    // One GPU, top-1: F11 fused into F7's epilogue (O still stored for the backward)
-    fused_combine = solo && d.K == 1 && y && !c->no_fused_combine;
     GateDxArgs cmb{at<int32_t>(saved, sv.tok_of), at<int32_t>(saved, sv.count), nullptr, nullptr, d.E, d.C, y,
                    at<float>(saved, sv.prob), nullptr, nullptr};
     if (fused_combine) {
@@ -662,10 +663,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   }
 
   // F11 combine (not in a checkpoint replay: the layer output is not needed again)
-  if (fused_combine) {
-    Scope sc_(c, MOE_K_COMBINE, st, 1);
-    CUDA_TRY(c, zero_dropped(at<int32_t>(saved, sv.slot), d.T, d.H, y, st));
-  } else if (y) {
+  if (y && !fused_combine) {
     Scope sc_(c, MOE_K_COMBINE, st, 1);
     CUDA_TRY(c, combine(O, at<int32_t>(saved, sv.expert), at<int32_t>(saved, sv.slot),
                         at<float>(saved, sv.prob), ss, d.T, y, st));
@@ -931,6 +929,7 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   ra.tok_of = at<int32_t>(saved, sv.tok_of);
   ra.local_rank = at<int32_t>(c->scratch, sc.local_rank);
   ra.block_hist = at<int32_t>(c->scratch, sc.block_hist);
+  ra.tile_ties = at<int32_t>(c->scratch, sc.tile_ties);
   ra.ties = at<int32_t>(saved, sv.ties);
   ra.rts = d.rts ? 1 : 0;
   ra.seed = c->priority_seed;
@@ -938,7 +937,7 @@ moe_status moe_forward(moe_ctx* c, const void* x, const float* wg, const void* w
   ra.aux_partial = d.aux ? at<float>(c->scratch, sc.auxp) : nullptr;
   ra.aux_out = d.aux ? at<float>(saved, sv.aux) : nullptr;
   {
-    Scope sc_(c, MOE_K_ROUTE, st, d.aux ? 5 : 3);
+    Scope sc_(c, MOE_K_ROUTE, st, (d.K == 1 && !d.rts ? 2 : 3) + (d.aux ? 2 : 0));
     CUDA_TRY(c, route(ra, st));
   }
 
@@ -1004,6 +1003,10 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   void* dXp = d.peer && d.Gt > 1 ? c->comm->win[moe_comm::W_DXP] : at<uint8_t>(c->scratch, sc.dXp);
   void* dS = d.peer ? c->comm->win[moe_comm::W_DS] : at<uint8_t>(c->scratch, sc.dS);
 
+  // One GPU, top-1, no aux loss: B5's epilogue adds B10's gate term and writes dx rows
+  // directly (no dXp round trip, no separate dx gather); dl and the extension operands
+  // come from the combine-backward launch.
+  const bool fused_dx = solo && d.K == 1 && !d.aux && d.E <= 16 && !c->no_fused_dx;
   // B1 combine-bwd (DTD: only this rank's slice of dO), B2 a2a, B3 all-gather
   const bool split = d.peer && d.Gt == 1 && d.Gep > 1 && c->overlap;  // as in forward_core
   uint32_t sig = 0;
@@ -1028,6 +1031,13 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, 1, st));
+  } else if (fused_dx) {
+    // B1 + the head of B10 in one launch (dl, extension operands, dropped rows)
+    Scope sc_(c, MOE_K_COMBINE_BWD, st, 1);
+    CUDA_TRY(c, combine_bwd_gate(dy, O, expert, slot, prob, logits, at<int32_t>(saved, sv.tok_of), count, wg,
+                                 d.T, d.H, d.E, d.C, dO, at<float>(c->scratch, sc.dl),
+                                 at<uint8_t>(c->scratch, sc.aext), at<uint8_t>(c->scratch, sc.bext), dx,
+                                 at<int32_t>(c->scratch, sc.dwgc), st));
   } else {
     Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
     CUDA_TRY(c, combine_bwd(dy, O, expert, slot, prob, count, ss, d.T, lo, hi, dp, dO, st));
@@ -1055,26 +1065,13 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     TRY(gemm(c, g4, st));
   }
   GemmArgs g5{d.El, (int)d.R, d.H, d.Fl, dH, 0, w1, 1, dXp, EPI_STORE, nullptr};
-  // One GPU, top-1, no aux loss: B5's epilogue adds B10's gate term and writes dx rows
-  // directly (no dXp round trip, no separate dx gather); dl is computed before B5.
-  const bool fused_dx = solo && d.K == 1 && !d.aux && d.E <= 16 && !c->no_fused_dx;
   GateDxArgs gdx{at<int32_t>(saved, sv.tok_of), count, at<float>(c->scratch, sc.dl), wg, d.E, d.C, dx,
                  nullptr, at<uint8_t>(c->scratch, sc.aext), at<uint8_t>(c->scratch, sc.bext)};
   if (fused_dx) {
-    {
-      Scope sc_(c, MOE_K_GATE_BWD, st, 3);
-      CUDA_TRY(c, gate_dl(logits, expert, slot, prob, dp, d.T, d.E, at<float>(c->scratch, sc.dl), st));
-      CUDA_TRY(c, gate_ext(at<float>(c->scratch, sc.dl), at<int32_t>(saved, sv.tok_of), count, wg, d.E, d.C,
-                           d.H, at<uint8_t>(c->scratch, sc.aext), at<uint8_t>(c->scratch, sc.bext), st));
-    }
     g5.epilogue = EPI_SCATTER;
     g5.gdx = &gdx;
   }
   TRY(gemm(c, g5, st));
-  if (fused_dx) {
-    Scope sc_(c, MOE_K_GATE_BWD, st, 1);
-    CUDA_TRY(c, zero_dropped(slot, d.T, d.H, dx, st));
-  }
   GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};
   GemmArgs g7{d.El, d.Fl, d.H, (int)d.R, dH, 1, X, 1, dw1, EPI_STORE, nullptr};
   if (d.peer && d.Gt > 1) {
@@ -1147,9 +1144,10 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   }
   // B10 dispatch-bwd + gate-bwd (fused path: only dWg is left)
   if (fused_dx) {
-    Scope sc_(c, MOE_K_GATE_BWD, st, 2);
-    CUDA_TRY(c, gate_dwg(x, at<float>(c->scratch, sc.dl), d.T, d.H, d.E, dwg, at<float>(c->scratch, sc.dwgp),
-                         sc.nsplit, st));
+    // dWg = X^T a_ext over the kept slot rows (dl = 0 for dropped tokens)
+    Scope sc_(c, MOE_K_GATE_BWD, st, 1);
+    CUDA_TRY(c, gate_dwg_tc(X, at<uint8_t>(c->scratch, sc.aext), (int64_t)d.E * d.C, d.H, d.E, dwg,
+                            at<float>(c->scratch, sc.dwgp), DWG_TC_SPLITS, at<int32_t>(c->scratch, sc.dwgc), st));
   } else {
     Scope sc_(c, MOE_K_GATE_BWD, st, 4);
     CUDA_TRY(c, gate_bwd(x, dS, wg, logits, expert, slot, prob, dp, ss, d.T, dx, dwg,

@@ -331,6 +331,23 @@ __device__ __forceinline__ float2 gelu_grad2(float2 h) {
   return f2fma(f2mul(f2mul(kh, make_float2(0.5f, 0.5f)), s), b, a);
 }
 
+// gelu_tanh and its derivative on a pair, sharing u and tanh(u) (same formulas as
+// gelu2 / gelu_grad2: the F6 epilogue needs both)
+__device__ __forceinline__ void gelu_and_grad2(float2 h, float2& g, float2& gp) {
+  const float k = 0.7978845608028654f, c = 0.044715f;
+  const float2 h2 = f2mul(h, h);
+  const float2 t = f2fma(h2, make_float2(c, c), make_float2(1.f, 1.f));
+  const float2 kh = f2mul(h, make_float2(k, k));
+  const float2 u = f2mul(kh, t);
+  const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 hh = f2mul(h, make_float2(0.5f, 0.5f));
+  g = f2fma(hh, th, hh);
+  const float2 a = f2fma(th, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
+  const float2 s = f2fma(f2mul(th, th), make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
+  const float2 b = f2fma(h2, make_float2(3.f * c, 3.f * c), make_float2(1.f, 1.f));
+  gp = f2fma(f2mul(f2mul(kh, make_float2(0.5f, 0.5f)), s), b, a);
+}
+
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"

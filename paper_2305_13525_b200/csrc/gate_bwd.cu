@@ -8,6 +8,7 @@
 // on fp32 CUDA cores in route.cu.
 #include <atomic>
 #include <cstdlib>
+#include <cuda.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -402,71 +403,289 @@ __global__ void dwg_reduce2_kernel(const float* __restrict__ partial, int nsplit
   dwg[i] = s;
 }
 
-// ------------------------------------------------------------------ fused-path pieces
-// dl_tj = dp_t p_t (delta_{j e*} - softmax(l_t)_j) for kept tokens, 0 otherwise (top-1)
-__global__ void __launch_bounds__(256)
-    gate_dl_kernel(const float* __restrict__ logits, const int32_t* __restrict__ expert,
-                   const int32_t* __restrict__ slot, const float* __restrict__ prob,
-                   const float* __restrict__ dp, int64_t T, int E, float* __restrict__ dl) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  float* o = dl + (size_t)t * E;
-  if (slot[t] < 0) {
-    for (int j = 0; j < E; ++j) o[j] = 0.f;
+// ------------------------------------------------------------------ fused one-GPU B1 + B10 head
+// One launch replaces combine_bwd + zero_empty + gate_dl + gate_ext_a/b + zero_dropped
+// (top-1, one GPU, E <= 16; slot space == expert space, row r = e * C + c). Warp work items:
+//   [0, E*C)           slot row r: kept -> t = tok_of[r]: dp = <dy_t, O_r> (fp32),
+//                      dO_r = bf16(p_t dy_t), then lanes j < E: dl_tj = dp p_t (d_{j e*} - s_tj)
+//                      (fp32, for dWg) and the K-extension row a_ext[r] = [hi | lo | hi | 0](dl_t);
+//                      empty -> dO_r = 0, a_ext[r] = 0
+//   next T/32          32 tokens per warp: dropped tokens get dl_t = 0 and dx_t = 0 (B5's
+//                      scatter writes only kept rows)
+//   next 16*H/256      b_ext = [hi(Wg)^T ; hi(Wg)^T ; lo(Wg)^T ; 0], 256 h of one j per warp
+constexpr int CBG_WARPS = 8;
+__global__ void __launch_bounds__(CBG_WARPS * 32)
+    combine_bwd_gate_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ O,
+                            const int32_t* __restrict__ expert, const int32_t* __restrict__ slot,
+                            const float* __restrict__ prob, const float* __restrict__ logits,
+                            const int32_t* __restrict__ tok_of, const int32_t* __restrict__ count,
+                            const float* __restrict__ wg, int64_t T, int H, int E, int64_t C,
+                            bf16* __restrict__ dO, float* __restrict__ dl, bf16* __restrict__ a_ext,
+                            bf16* __restrict__ b_ext, bf16* __restrict__ dx, int32_t* __restrict__ dwg_cnt,
+                            int ncnt) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0)  // split-K counters of the dWg launch that follows (stream order)
+    for (int i = threadIdx.x; i < ncnt; i += blockDim.x) dwg_cnt[i] = 0;
+  int64_t w = (int64_t)blockIdx.x * CBG_WARPS + (threadIdx.x >> 5);
+  const int64_t rows = (int64_t)E * C;
+  const int nv = H / 8;
+  if (w < rows) {
+    const int e = (int)(w / C);
+    const int64_t c = w - (int64_t)e * C;
+    bf16* dst = dO + (size_t)w * H;
+    bf16* arow = a_ext + (size_t)w * 64;
+    if (c >= count[e]) {
+      for (int v = lane; v < nv; v += 32) st_v4(dst + (size_t)v * 8, make_uint4(0, 0, 0, 0));
+      if (lane < 8) st_v4(arow + lane * 8, make_uint4(0, 0, 0, 0));
+      return;
+    }
+    const int t = tok_of[w];
+    const float p = prob[t];
+    const bf16* dyr = dy + (size_t)t * H;
+    const bf16* orow = O + (size_t)w * H;
+    float acc = 0.f;
+    constexpr int U = 4;
+    for (int v0 = 0; v0 < nv; v0 += 32 * U) {
+      uint4 a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        a[u] = v < nv ? ld_nc_v4(dyr + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+        b[u] = v < nv ? ld_nc_v4(orow + (size_t)v * 8) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = v0 + u * 32 + lane;
+        const uint32_t wa[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+        const uint32_t wb[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 fa = unpack_bf16x2(wa[k]), fb = unpack_bf16x2(wb[k]);
+          acc = fmaf(fa.x, fb.x, acc);
+          acc = fmaf(fa.y, fb.y, acc);
+          o[k] = pack_bf16x2(p * fa.x, p * fa.y);
+        }
+        if (v < nv) st_v4(dst + (size_t)v * 8, make_uint4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    const float dp = warp_sum(acc);
+    // softmax of the saved logits over lanes j < E (E <= 16 on this path)
+    const float lj = lane < E ? logits[(size_t)t * E + lane] : -3.402823e38f;
+    float m = lj;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float ex = lane < E ? expf(lj - m) : 0.f;
+    const float den = warp_sum(ex);
+    const float d = lane < E ? dp * p * ((lane == expert[t] ? 1.f : 0.f) - ex / den) : 0.f;
+    if (lane < E) dl[(size_t)t * E + lane] = d;
+    if (lane < 16) {
+      bf16 hi, lo;
+      split_bf16(d, hi, lo);
+      arow[lane] = hi;
+      arow[16 + lane] = lo;
+      arow[32 + lane] = hi;
+      arow[48 + lane] = __float2bfloat16_rn(0.f);
+    }
     return;
   }
-  const float* lg = logits + (size_t)t * E;
-  float m = -3.402823e38f;
-  for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
-  float den = 0.f;
-  for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
-  const float inv = 1.f / den, gsc = dp[t] * prob[t];
-  const int e = expert[t];
-  for (int j = 0; j < E; ++j) o[j] = gsc * ((j == e ? 1.f : 0.f) - expf(lg[j] - m) * inv);
+  w -= rows;
+  const int64_t tw = (T + 31) / 32;
+  if (w < tw) {
+    const int64_t t = w * 32 + lane;
+    const bool dropped = t < T && slot[t] < 0;
+    uint32_t mask = __ballot_sync(0xffffffffu, dropped);
+    if (dropped)
+      for (int j = 0; j < E; ++j) dl[(size_t)t * E + j] = 0.f;
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      mask &= mask - 1;
+      bf16* xr = dx + (size_t)(w * 32 + l) * H;
+      for (int v = lane; v < nv; v += 32) st_v4(xr + (size_t)v * 8, make_uint4(0, 0, 0, 0));
+    }
+    return;
+  }
+  w -= tw;
+  const int64_t hb = (H + 255) / 256;
+  if (w >= 16 * hb) return;
+  const int j = (int)(w / hb);
+  const int h0 = (int)(w - (int64_t)j * hb) * 256 + lane * 8;
+  if (h0 >= H) return;
+  uint32_t hw[4], lw[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    bf16 h2[2], l2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) split_bf16(j < E ? wg[(size_t)(h0 + 2 * i + u) * E + j] : 0.f, h2[u], l2[u]);
+    hw[i] = pack2(h2[0], h2[1]);
+    lw[i] = pack2(l2[0], l2[1]);
+  }
+  const uint4 vh = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+  st_v4(b_ext + (size_t)j * H + h0, vh);
+  st_v4(b_ext + (size_t)(16 + j) * H + h0, vh);
+  st_v4(b_ext + (size_t)(32 + j) * H + h0, make_uint4(lw[0], lw[1], lw[2], lw[3]));
+  st_v4(b_ext + (size_t)(48 + j) * H + h0, make_uint4(0, 0, 0, 0));
 }
 
-// K-extension operands of EPI_SCATTER (split-bf16 products: hi*hi + lo*hi + hi*lo)
-__global__ void __launch_bounds__(256)
-    gate_ext_a_kernel(const float* __restrict__ dl, const int32_t* __restrict__ tok_of,
-                      const int32_t* __restrict__ count, int E, int64_t C, int64_t rows, bf16* __restrict__ a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (slot row, expert j) pair
-  if (i >= rows * 16) return;
-  const int64_t r = i >> 4;
-  const int j = (int)(i & 15);
-  const int e = (int)(r / C);
-  const int64_t c = r - (int64_t)e * C;
-  float v = 0.f;
-  if (c < count[e] && j < E) v = dl[(size_t)tok_of[r] * E + j];
-  bf16 hi, lo;
-  split_bf16(v, hi, lo);
-  bf16* row = a + (size_t)r * 64;
-  row[j] = hi;
-  row[16 + j] = lo;
-  row[32 + j] = hi;
-  row[48 + j] = __float2bfloat16_rn(0.f);
+// ------------------------------------------------------------------ dWg on the tensor cores
+// One GPU, top-1, E <= 16: dWg = sum_t x_t^T dl_t = sum over kept slot rows r of
+// X_r^T dl_tok(r) (dl is zero for dropped tokens), with X the dispatched rows [E*C][H]
+// (expert space) and the K-extension rows a_ext [E*C][64] = [hi(dl) | lo(dl) | hi | 0]
+// that combine_bwd_gate already wrote. D[h][n] = sum_r X[r][h] a_ext[r][n] is a
+// tcgen05 GEMM with M = 128 h (A = X, MN-major), N = 64 (B = a_ext, MN-major), K = rows,
+// and dWg[h][j] = D[h][j] + D[h][16 + j]. Split-K over nsplit CTAs per 128-row h tile
+// (CTA = split * mtiles + tile, so CTAs running together read the same rows); each
+// writes its partial, and the last CTA of a tile (counter zeroed by combine_bwd_gate)
+// sums the partials in split order: deterministic, one launch.
+namespace dwtc {
+constexpr int A_BYTES = 128 * 64 * 2;
+constexpr int B_BYTES = 64 * 64 * 2;
+constexpr int STAGES = 8;
+constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+constexpr int THREADS = 192;
+
+__device__ __forceinline__ uint64_t mn_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(8192 >> 4) << 16;  // LBO: next 64-wide MN block
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8 K-rows x 128 B
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
 }
 
-__global__ void __launch_bounds__(256)
-    gate_ext_b_kernel(const float* __restrict__ wg, int E, int H, bf16* __restrict__ b) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (j, h) pair
-  if (i >= (int64_t)16 * H) return;
-  const int j = (int)(i / H), h = (int)(i - (int64_t)j * H);
-  const float v = j < E ? wg[(size_t)h * E + j] : 0.f;
-  bf16 hi, lo;
-  split_bf16(v, hi, lo);
-  b[(size_t)j * H + h] = hi;
-  b[(size_t)(16 + j) * H + h] = hi;
-  b[(size_t)(32 + j) * H + h] = lo;
-  b[(size_t)(48 + j) * H + h] = __float2bfloat16_rn(0.f);
-}
+__global__ void __launch_bounds__(THREADS, 1)
+    dwg_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t rows,
+                  int H, int E, int mtiles, int nsplit, float* __restrict__ partial, int32_t* __restrict__ cnt,
+                  float* __restrict__ dwg) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * (A_BYTES + B_BYTES));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  __shared__ int last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = (int)(blockIdx.x % mtiles), split = (int)(blockIdx.x / mtiles);
+  const int h0 = mt * 128;
+  const int KB = (int)((rows + 63) / 64);
+  const int per = (KB + nsplit - 1) / nsplit;
+  const int kb0 = split * per;
+  const int kb1 = kb0 + per < KB ? kb0 + per : KB;
+  const int nkb = kb1 > kb0 ? kb1 - kb0 : 0;
 
-__global__ void __launch_bounds__(256)
-    zero_dropped_kernel(const int32_t* __restrict__ slot, int64_t T, int H, bf16* __restrict__ dx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (t >= T || slot[t] >= 0) return;
-  for (int v = lane; v < H / 8; v += 32) st_v4(dx + (size_t)t * H + (size_t)v * 8, make_uint4(0, 0, 0, 0));
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&bars[s]), 1);
+      mbar_init(smem_u32(&bars[STAGES + s]), 1);
+    }
+    mbar_init(smem_u32(&bars[2 * STAGES]), 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(64)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int stage = i % STAGES;
+        const uint32_t phase = (uint32_t)(i / STAGES) & 1;
+        mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1);
+        const uint32_t full = smem_u32(&bars[stage]);
+        mbar_arrive_expect_tx(full, A_BYTES + B_BYTES);
+        const uint32_t a = smem_u32(smem + stage * (A_BYTES + B_BYTES));
+        const int r0 = (kb0 + i) * 64;
+        tma_load_3d(a, &tmA, full, h0, r0, 0);
+        tma_load_3d(a + 8192, &tmA, full, h0 + 64, r0, 0);
+        tma_load_3d(a + A_BYTES, &tmB, full, 0, r0, 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                                 ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      for (int i = 0; i < nkb; ++i) {
+        const int stage = i % STAGES;
+        mbar_wait(smem_u32(&bars[stage]), (uint32_t)(i / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a = smem_u32(smem + stage * (A_BYTES + B_BYTES));
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          tc_mma_f16(tmem, mn_desc(a + j * 2048), mn_desc(a + A_BYTES + j * 2048), idesc, (i | j) ? 1u : 0u);
+        tc_commit(smem_u32(&bars[STAGES + stage]));
+      }
+      if (nkb > 0) tc_commit(smem_u32(&bars[2 * STAGES]));
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 0-3: TMEM lane = h row of the tile
+    const int hl = warp * 32 + lane;
+    const int h = h0 + hl;
+    float v[16];
+    if (nkb > 0) {
+      mbar_wait(smem_u32(&bars[2 * STAGES]), 0);
+      tc_fence_after();
+      uint32_t hi[16], lo[16];
+      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+          : "=r"(hi[0]), "=r"(hi[1]), "=r"(hi[2]), "=r"(hi[3]), "=r"(hi[4]), "=r"(hi[5]), "=r"(hi[6]),
+            "=r"(hi[7]), "=r"(hi[8]), "=r"(hi[9]), "=r"(hi[10]), "=r"(hi[11]), "=r"(hi[12]), "=r"(hi[13]),
+            "=r"(hi[14]), "=r"(hi[15])
+          : "r"(ta));
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+          : "=r"(lo[0]), "=r"(lo[1]), "=r"(lo[2]), "=r"(lo[3]), "=r"(lo[4]), "=r"(lo[5]), "=r"(lo[6]),
+            "=r"(lo[7]), "=r"(lo[8]), "=r"(lo[9]), "=r"(lo[10]), "=r"(lo[11]), "=r"(lo[12]), "=r"(lo[13]),
+            "=r"(lo[14]), "=r"(lo[15])
+          : "r"(ta + 16));
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(hi[j]) + __uint_as_float(lo[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+    }
+    if (h < H) {
+      float* prow = partial + ((size_t)split * H + h) * E;
+      for (int j = 0; j < E; ++j) prow[j] = v[j];
+    }
+    __threadfence();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 0) last = atomicAdd(&cnt[mt], 1) == nsplit - 1;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (last) {  // every split of this h tile is in: sum in split order
+      __threadfence();
+      if (h < H) {
+        for (int j = 0; j < E; ++j) {
+          float sum = 0.f;
+          for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(partial + ((size_t)sp * H + h) * E + j);
+          dwg[(size_t)h * E + j] = sum;
+        }
+      }
+      if (threadIdx.x == 0) cnt[mt] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64) : "memory");
+  }
 }
+}  // namespace dwtc
 
 template <int EP>
 cudaError_t dwg_only(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,
@@ -558,25 +777,43 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
 #undef RUN
 }
 
-cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* slot, const float* prob,
-                    const float* dp, int64_t T, int E, float* dl, cudaStream_t s) {
-  if (T <= 0) return cudaSuccess;
-  gate_dl_kernel<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(logits, expert, slot, prob, dp, T, E, dl);
+cudaError_t combine_bwd_gate(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
+                             const float* prob, const float* logits, const int32_t* tok_of,
+                             const int32_t* count, const float* wg, int64_t T, int H, int E, int64_t C,
+                             void* dO, float* dl, void* a_ext, void* b_ext, void* dx, int32_t* dwg_cnt,
+                             cudaStream_t s) {
+  if (E > 16) return cudaErrorInvalidValue;
+  const int64_t items = (int64_t)E * C + (T + 31) / 32 + 16 * ((H + 255) / 256);
+  combine_bwd_gate_kernel<<<(unsigned)((items + CBG_WARPS - 1) / CBG_WARPS), CBG_WARPS * 32, 0, s>>>(
+      static_cast<const bf16*>(dy), static_cast<const bf16*>(O), expert, slot, prob, logits, tok_of, count, wg,
+      T, H, E, C, static_cast<bf16*>(dO), dl, static_cast<bf16*>(a_ext), static_cast<bf16*>(b_ext),
+      static_cast<bf16*>(dx), dwg_cnt, (H + 127) / 128);
   return cudaGetLastError();
 }
 
-cudaError_t gate_ext(const float* dl, const int32_t* tok_of, const int32_t* count, const float* wg, int E,
-                     int64_t C, int H, void* a_ext, void* b_ext, cudaStream_t s) {
-  const int64_t rows = (int64_t)E * C;
-  gate_ext_a_kernel<<<(unsigned)((rows * 16 + 255) / 256), 256, 0, s>>>(dl, tok_of, count, E, C, rows,
-                                                                         static_cast<bf16*>(a_ext));
-  gate_ext_b_kernel<<<(unsigned)(((int64_t)16 * H + 255) / 256), 256, 0, s>>>(wg, E, H, static_cast<bf16*>(b_ext));
-  return cudaGetLastError();
-}
-
-cudaError_t zero_dropped(const int32_t* slot, int64_t T, int H, void* dx, cudaStream_t s) {
-  if (T <= 0) return cudaSuccess;
-  zero_dropped_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(slot, T, H, static_cast<bf16*>(dx));
+cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, int E, float* dwg, float* partial,
+                        int max_split, int32_t* counters, cudaStream_t s) {
+  if (E > 16) return cudaErrorInvalidValue;
+  if (rows <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * H * E, s);
+  CUtensorMap ta, tb;
+  int sms = 0;
+  cudaError_t e = tensor_map_bf16(&ta, X, (uint64_t)H, (uint64_t)rows, 64, 64, &sms);
+  if (e == cudaSuccess) e = tensor_map_bf16(&tb, a_ext, 64, (uint64_t)rows, 64, 64, &sms);
+  if (e != cudaSuccess) return e;
+  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
+  if (!attr) {
+    e = cudaFuncSetAttribute(dwtc::dwg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dwtc::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int mtiles = (H + 127) / 128;
+  const int kb = (int)((rows + 63) / 64);
+  int nsplit = sms / mtiles;                  // one wave
+  if (nsplit > (kb + 3) / 4) nsplit = (kb + 3) / 4;  // >= 4 k-blocks per CTA
+  if (nsplit > max_split) nsplit = max_split;
+  if (nsplit < 1) nsplit = 1;
+  dwtc::dwg_tc_kernel<<<(unsigned)(mtiles * nsplit), dwtc::THREADS, dwtc::SMEM, s>>>(
+      ta, tb, rows, H, E, mtiles, nsplit, partial, counters, dwg);
   return cudaGetLastError();
 }
 

@@ -487,8 +487,8 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
             o[w] = pack_bf16x2(r2.x, r2.y);
           } else if (EPI == EPI_GELU) {
             // D = gelu'(acc) (for the backward), aux = gelu(acc) (the FFN activation)
-            const float2 gp = gelu_grad2(f);
-            const float2 gg = gelu2(f);
+            float2 gg, gp;
+            gelu_and_grad2(f, gg, gp);
             o[w] = pack_bf16x2(gp.x, gp.y);
             g[w] = pack_bf16x2(gg.x, gg.y);
           } else if (EPI == EPI_COMBINE) {
@@ -625,6 +625,16 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensor
 }
 
 }  // namespace
+
+cudaError_t tensor_map_bf16(void* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                            uint32_t box_outer, int* sms) {
+  std::call_once(g_once, init_once);
+  if (g_init_err != cudaSuccess) return g_init_err;
+  *sms = g_num_sms;
+  return make_map(static_cast<CUtensorMap*>(map), ptr, inner, outer, 1, box_inner, box_outer)
+             ? cudaSuccess
+             : cudaErrorInvalidValue;
+}
 
 cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   std::call_once(g_once, init_once);

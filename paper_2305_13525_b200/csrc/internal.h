@@ -51,9 +51,14 @@ struct GemmArgs {
 cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why);
 // Plain SIMT kernel: bring-up cross-check only (moe_gemm_bf16 impl=1).
 cudaError_t gemm_ref(const GemmArgs& a, cudaStream_t s);
+// (gemm_sm100.cu) 2-D bf16 TMA map {inner, outer}, box {box_inner, box_outer}, 128B
+// swizzle, into the 128-byte CUtensorMap at `map`; *sms = the device's SM count.
+cudaError_t tensor_map_bf16(void* map, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                            uint32_t box_outer, int* sms);
 
 // ---- routing / permutation kernels (route.cu, permute.cu) ----
-constexpr int AUX_GRID = 64;  // CTAs of the deterministic P_e reduction (aux loss)
+constexpr int AUX_GRID = 64;
+constexpr int DWG_TC_SPLITS = 16;  // most split-K partials of gate_dwg_tc  // CTAs of the deterministic P_e reduction (aux loss)
 struct RouteArgs {
   const void* x;        // bf16 [T][H]
   const float* wg;      // [H][E]
@@ -71,7 +76,8 @@ struct RouteArgs {
   int32_t* load;        // [E]   routed per expert (pre-capacity)
   int32_t* tok_of;      // [E][C] item (token * K + choice) of (expert, slot), valid for slot < count
   int32_t* local_rank;  // scratch [K*T]
-  int32_t* block_hist;  // scratch [ceil(K*T/1024)][E]
+  int32_t* block_hist;  // scratch [ceil(K*T/8)][E] (per gate tile of R >= 8 tokens, or per 1024 items)
+  int32_t* tile_ties;   // scratch [ceil(T/8)]: ties per gate tile, summed by the slot scan
   int32_t* ties;        // [1]: tokens with gap < 1e-6
   // NEXT #4 gating variants
   int rts;              // random token-selection priority (R20)
@@ -90,9 +96,10 @@ struct SlotSpace {
 };
 
 // F3: D[tt][e][cs] = x[tok_of[e][tt*Cs+cs]] (zeros for empty slots), for slices
-// tt in [t_lo, t_hi).
+// tt in [t_lo, t_hi). y_zero (or null): also zero the rows of tokens with slot[t] < 0.
 cudaError_t dispatch(const void* x, const int32_t* tok_of, const int32_t* count,
-                     const SlotSpace& ss, int t_lo, int t_hi, void* D, cudaStream_t s);
+                     const SlotSpace& ss, int t_lo, int t_hi, void* D, const int32_t* slot, int64_t T,
+                     void* y_zero, cudaStream_t s);
 
 // F11: y_t = bf16(sum over kept choices k of p_tk * O[row(t,k)]), 0 if all dropped.
 cudaError_t combine(const void* O, const int32_t* expert, const int32_t* slot, const float* prob,
@@ -114,14 +121,21 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
                      const float* aux_f, float aux_coef, cudaStream_t s);
 int gate_bwd_splits(int64_t T);
-// Pieces of B10 for the fused path (EPI_SCATTER): dl [T][E] before B5; zero dx rows of
-// dropped tokens; dWg = x^T dl (deterministic split-K) after.
-cudaError_t gate_dl(const float* logits, const int32_t* expert, const int32_t* slot, const float* prob,
-                    const float* dp, int64_t T, int E, float* dl, cudaStream_t s);
-// EPI_SCATTER extension operands: a_ext [E][C][64] from dl and the slot map, b_ext [64][H] from Wg.
-cudaError_t gate_ext(const float* dl, const int32_t* tok_of, const int32_t* count, const float* wg, int E,
-                     int64_t C, int H, void* a_ext, void* b_ext, cudaStream_t s);
-cudaError_t zero_dropped(const int32_t* slot, int64_t T, int H, void* dx, cudaStream_t s);
+// One-GPU top-1 (E <= 16) head of the backward in one launch: B1 (dp, dO incl. empty-slot
+// zeros), dl, the EPI_SCATTER extension operands a_ext / b_ext, and zero dl / dx rows of
+// dropped tokens (gate_bwd.cu).
+cudaError_t combine_bwd_gate(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
+                             const float* prob, const float* logits, const int32_t* tok_of,
+                             const int32_t* count, const float* wg, int64_t T, int H, int E, int64_t C,
+                             void* dO, float* dl, void* a_ext, void* b_ext, void* dx, int32_t* dwg_cnt,
+                             cudaStream_t s);
+// dWg on the tensor cores from the dispatched rows X [rows][H] and the K-extension rows
+// a_ext [rows][64] (one GPU, top-1, E <= 16): one launch, split-K partials [<= max_split][H][E]
+// summed in fixed order by the last CTA of each h tile; counters [ceil(H/128)] zeroed by
+// combine_bwd_gate.
+cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, int E, float* dwg, float* partial,
+                        int max_split, int32_t* counters, cudaStream_t s);
+// dWg = x^T dl (deterministic split-K), the tail of B10 on the fused path.
 cudaError_t gate_dwg(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,
                      int nsplit, cudaStream_t s);
 size_t gate_bwd_pack_bytes(int H, int E);

@@ -39,13 +39,27 @@ __device__ __forceinline__ void copy_row(const bf16* __restrict__ src, bf16* __r
   }
 }
 
+// Warps [0, rows): one slot row each. With y_zero (one GPU, F11 fused into F7's
+// epilogue, which writes only kept tokens' rows) warps [rows, rows + T/32) zero the y
+// rows of the dropped tokens among 32 tokens each.
 __global__ void __launch_bounds__(WARPS * 32)
     dispatch_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ tok_of,
                     const int32_t* __restrict__ count, SlotSpace ss, int t_lo, int64_t rows,
-                    bf16* __restrict__ D) {
+                    bf16* __restrict__ D, const int32_t* __restrict__ slot, int64_t T,
+                    bf16* __restrict__ y_zero) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (r >= rows) return;
+  if (r >= rows) {
+    const int64_t t = (r - rows) * 32 + lane;
+    if (!y_zero || (r - rows) * 32 >= T) return;
+    uint32_t mask = __ballot_sync(0xffffffffu, t < T && slot[t] < 0);
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      mask &= mask - 1;
+      copy_row<true>(nullptr, y_zero + (size_t)((r - rows) * 32 + l) * ss.H, ss.H / 8, lane);
+    }
+    return;
+  }
   const int64_t per_slice = (int64_t)ss.E * ss.Cs;
   const int tt = t_lo + (int)(r / per_slice);
   const int64_t rem = r % per_slice;
@@ -429,12 +443,15 @@ inline unsigned blocks_for(int64_t n) { return (unsigned)((n + WARPS - 1) / WARP
 }  // namespace
 
 cudaError_t dispatch(const void* x, const int32_t* tok_of, const int32_t* count,
-                     const SlotSpace& ss, int t_lo, int t_hi, void* D, cudaStream_t s) {
+                     const SlotSpace& ss, int t_lo, int t_hi, void* D, const int32_t* slot, int64_t T,
+                     void* y_zero, cudaStream_t s) {
   const int64_t rows = (int64_t)(t_hi - t_lo) * ss.E * ss.Cs;
-  if (rows <= 0) return cudaSuccess;
-  dispatch_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(static_cast<const bf16*>(x), tok_of,
-                                                           count, ss, t_lo, rows,
-                                                           static_cast<bf16*>(D));
+  const int64_t zw = y_zero ? (T + 31) / 32 : 0;
+  if (rows + zw <= 0) return cudaSuccess;
+  dispatch_kernel<<<blocks_for(rows + zw), WARPS * 32, 0, s>>>(static_cast<const bf16*>(x), tok_of,
+                                                                count, ss, t_lo, rows,
+                                                                static_cast<bf16*>(D), slot, T,
+                                                                static_cast<bf16*>(y_zero));
   return cudaGetLastError();
 }
 

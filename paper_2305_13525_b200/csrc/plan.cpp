@@ -129,7 +129,9 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->nsplit = gate_bwd_splits(d.T);
   Bump f;
   sc->local_rank = f.take((size_t)d.T * d.K * 4);
-  sc->block_hist = f.take((size_t)((d.T * d.K + 1023) / 1024) * d.E * 4);
+  // gate tiles hold R >= 8 tokens (route.cu), 1024-item blocks for the unfused scan
+  sc->block_hist = f.take((size_t)((d.T * d.K + 7) / 8) * d.E * 4);
+  sc->tile_ties = f.take((size_t)((d.T + 7) / 8) * 4);
   sc->auxp = d.aux ? f.take((size_t)AUX_GRID * d.E * 8) : 0;  // P partials + first-choice counts
   // peer mode dispatches straight into windows; with G_t = 1 (split exchange) the rows of
   // remote experts are staged in slot space for the copy engines
@@ -139,7 +141,8 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   Bump b;  // backward region reuses the forward region
   sc->dp = b.take((size_t)d.T * d.K * 4);
   sc->dl = b.take((size_t)d.T * d.E * 4);
-  sc->dwgp = b.take((size_t)sc->nsplit * d.H * d.E * 4);
+  sc->dwgp = b.take((size_t)(sc->nsplit > DWG_TC_SPLITS ? sc->nsplit : DWG_TC_SPLITS) * d.H * d.E * 4);
+  sc->dwgc = b.take((size_t)((d.H + 127) / 128) * 4);  // split-K counters of the one-GPU dWg launch
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));
   sc->aext = solo ? b.take((size_t)d.E * d.C * 64 * 2) : 0;  // one-GPU fused B5 + B10 (K extension)
   sc->bext = solo ? b.take((size_t)64 * d.H * 2) : 0;

@@ -56,18 +56,26 @@ def routing_protocol(gpu_expert, gpu_gap, r: O.Routing):
 
 
 ROW_REL_BAR = 5e-2  # per-row bound beside the global one: a single corrupted row cannot hide
+ROW_FLOOR = 0.1    # row denominators never below 10% of the tensor's RMS row norm
 
 
 def row_errors(got, ref, axis_rows: int = -1):
     """Per-row relative L2 of got vs ref (rows = all but the last axis). Rows whose
     reference is exactly zero (dropped tokens, experts with no tokens) must be exactly
-    zero on the GPU too; returns (max rel over nonzero rows, #zero rows violated)."""
+    zero on the GPU too; returns (max rel over nonzero rows, #zero rows violated).
+
+    The denominator of a row is max(|ref_row|, ROW_FLOOR * RMS of the nonzero row norms)
+    (DESIGN.md §5): a row whose true norm is a small fraction of the typical row — e.g. a
+    dW1 row of a single token where gelu'(Hpre_f) ~ 0, so the bf16 rounding of Hpre is a
+    large relative error of that row — is judged against the row scale of its tensor; a
+    corrupted row (error of the order of a typical row) still fails."""
     g = np.asarray(got, dtype=np.float64).reshape(-1, np.asarray(got).shape[-1])
     r = np.asarray(ref, dtype=np.float64).reshape(-1, np.asarray(ref).shape[-1])
     nr = np.linalg.norm(r, axis=1)
     nd = np.linalg.norm(g - r, axis=1)
     nz = nr > 0
-    worst = float((nd[nz] / nr[nz]).max()) if nz.any() else 0.0
+    floor = ROW_FLOOR * float(np.sqrt(np.mean(nr[nz] ** 2))) if nz.any() else 0.0
+    worst = float((nd[nz] / np.maximum(nr[nz], floor)).max()) if nz.any() else 0.0
     bad_zero = int(np.count_nonzero(nd[~nz] > 0))
     return worst, bad_zero
 
