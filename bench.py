@@ -173,6 +173,55 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NvlinkCounter:
+    """NVLink data bytes sent / received by this rank's GPU (NVML field counters, summed
+    over links) around the timed region: the link-level evidence for the exchange bytes
+    the library's ledger claims. None where NVML exposes no counter."""
+    FIELDS = (("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX", 1024,
+               "NVML throughput data counters (KiB)"),
+              ("NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 1,
+               "NVML link byte counters"))
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.links = []
+            for link in range(18):
+                try:
+                    if pynvml.nvmlDeviceGetNvLinkState(self.h, link) == pynvml.NVML_FEATURE_ENABLED:
+                        self.links.append(link)
+                except Exception:
+                    pass
+            for tx, rx, unit, what in self.FIELDS:
+                ids = [(getattr(pynvml, tx), l) for l in self.links] + [(getattr(pynvml, rx), l) for l in self.links]
+                vals = pynvml.nvmlDeviceGetFieldValues(self.h, ids)
+                if self.links and all(v.nvmlReturn == 0 for v in vals):
+                    self.ids, self.unit, self.what, self.ok = ids, unit, what, True
+                    break
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        if not self.ok:
+            return None
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, self.ids)
+        n = len(self.links)
+        tx = sum(int(v.value.ullVal) for v in vals[:n]) * self.unit
+        rx = sum(int(v.value.ullVal) for v in vals[n:]) * self.unit
+        return tx, rx
+
+    def delta(self, a, b, steps):
+        if a is None or b is None:
+            return {"unavailable": "NVML returns NOT_SUPPORTED for every NVLink byte counter on this "
+                                   "system (tools/nvlink_probe.py); exchange bytes are the ledger's"}
+        return {"tx_bytes_per_step": (b[0] - a[0]) / steps, "rx_bytes_per_step": (b[1] - a[1]) / steps,
+                "links": len(self.links), "source": self.what}
+
+
 def cpu_oracle_step(shape_t, sample_tokens, state):
     """One oracle fwd+bwd on a bounded token sample (same shapes; C scaled with T)."""
     from oracle import moe_oracle as O
@@ -307,8 +356,10 @@ def main():
     layer.moe_stats_reset()
     clocks = ClockSampler(local)
     clocks.start()
+    nvl = NvlinkCounter(local) if world > 1 else None
     time.sleep(0.3)
     barrier()
+    nvl_a = nvl.read() if nvl else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
@@ -318,6 +369,7 @@ def main():
     marks[args.steps].record(stream)
     e1.record(stream)
     barrier()
+    nvl_b = nvl.read() if nvl else None
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
@@ -519,7 +571,8 @@ def main():
                           "transfer_ms_per_step": ex_ms, "egress_GB/s": gbs,
                           "peak_GB/s": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                           "frac": gbs / 770.0 if gbs else None, "time_basis": basis,
-                          "exposed_comm_ms_per_step": per_class["comm"]}
+                          "exposed_comm_ms_per_step": per_class["comm"],
+                          "nvlink_rank0": nvl.delta(nvl_a, nvl_b, args.steps) if nvl else None}
         print(json.dumps(out), flush=True)
     layer.close()
     if dist is not None:

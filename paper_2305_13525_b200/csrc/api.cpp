@@ -11,6 +11,7 @@
 // DTD feed the expert GEMMs the same rows in the same positions.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -25,6 +26,8 @@
 #include "../../include/moe_optim.h"
 #include "internal.h"
 #include "comm.h"
+
+#include <nvtx3/nvToolsExt.h>
 #include "plan.h"
 
 using namespace moe;
@@ -108,16 +111,22 @@ cudaEvent_t take_event(moe_ctx* c) {
 
 // Counts this library's kernel launches per class and, with MOE_F_TIMING,
 // brackets the class's work with CUDA events on the launching stream.
+// One kernel class of the path: launch count, CUDA events (MOE_F_TIMING) and an NVTX
+// range named after the class (host-side; header-only NVTX3, a no-op without a tool).
+const char* const kClassNames[8] = {"moe.route", "moe.dispatch", "moe.gemm", "moe.combine",
+                                    "moe.combine_bwd", "moe.gate_bwd", "moe.comm", "moe.xfer"};
 struct Scope {
   moe_ctx* c;
   int cls;
   cudaStream_t st;
   cudaEvent_t a = nullptr;
   Scope(moe_ctx* c_, int cls_, cudaStream_t st_, int kernels) : c(c_), cls(cls_), st(st_) {
+    nvtxRangePushA(kClassNames[cls]);
     c->stats.kernel_launches[cls] += kernels;
     if (c->timing && (a = take_event(c)) != nullptr) cudaEventRecord(a, st);
   }
   ~Scope() {
+    nvtxRangePop();
     if (!a) return;
     cudaEvent_t b = take_event(c);
     if (!b) { c->pool.push_back(a); return; }

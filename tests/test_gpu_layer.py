@@ -266,3 +266,27 @@ def test_fused_combine_matches_separate_kernel(monkeypatch):
         np.testing.assert_array_equal(a[k], b[k])
     assert rel_l2(a["y"], b["y"]) < 3e-3
     check_parity(inp, a, 1.0)
+
+
+@pytest.mark.parametrize("T,H,E", [(16384, 2048, 16), (4096, 4096, 16), (4096, 2560, 32), (3000, 2048, 64),
+                                   (1000, 128, 5)])
+def test_gate_logit_error(T, H, E):
+    """F1 on the tensor cores (Wg split hi + mid + lo, fp32 TMEM accumulation in K chunks):
+    the saved logits (first region of the saved blob, plan.cpp make_layouts) against the
+    float64 x . Wg of the oracle. Bound 2.5e-7 absolute: 4x inside the 1e-6 tie threshold
+    of BASELINE.json, so routing outside logged ties is decided exactly as in the oracle."""
+    shape = synth.LayerShape("gate", T, H, 256, E)
+    x_bits = synth.make_x(shape)
+    wg = synth.make_wg(shape)
+    cfg = MoEConfig(T, H, 256, E, 1.0, 1, 1, True, 1)
+    layer = MoELayer(cfg)
+    x = bf16_tensor(x_bits)
+    w1 = torch.zeros((E, 256, H), dtype=torch.bfloat16, device="cuda")
+    w2 = torch.zeros((E, H, 256), dtype=torch.bfloat16, device="cuda")
+    y, saved = layer.moe_forward(x, torch.from_numpy(wg).cuda(), w1, w2)
+    torch.cuda.synchronize()
+    got = saved[: T * E * 4].view(torch.float32).reshape(T, E).cpu().numpy().astype(np.float64)
+    layer.close()
+    ref = O.decode_bf16(x_bits) @ wg.astype(np.float64)
+    err = np.abs(got - ref).max()
+    assert err <= 2.5e-7, err
