@@ -320,8 +320,8 @@ const char* moe_last_error_detail(void);
  *               (the forward FFN GEMM: A for the second GEMM, G = gelu'(Hpre) for B4)
  *   epilogue 2: D = bf16(acc * aux), aux = G bf16 [batch][M][N] (read) (dGeLU)
  *   impl 0: tcgen05 CTA-pair kernel (cta_group::2, the product path);
- *   impl 2: tcgen05 single-CTA kernel; impl 1: plain SIMT reference kernel
- *   (bring-up cross-check only; never used by moe_forward/backward). */
+ *   impl 1: plain SIMT reference kernel (bring-up cross-check only; never used
+ *   by moe_forward/backward); anything else: MOE_ERR_UNSUPPORTED. */
 moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn,
                          const void* B, int b_mn, void* D, int epilogue, void* aux,
                          int impl, void* stream);

@@ -1290,7 +1290,7 @@ moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn
   if (!aligned16(A) || !aligned16(B) || !aligned16(D) || (aux && !aligned16(aux)))
     return fail(MOE_ERR_ALIGN, "operands must be 16-byte aligned");
   GemmArgs g{batch, M, N, K, A, a_mn ? 1 : 0, B, b_mn ? 1 : 0, D, epilogue, aux};
-  g.variant = impl == 2 ? 1 : 0;
+  if (impl != 0 && impl != 1) return fail(MOE_ERR_UNSUPPORTED, "impl must be 0 (tcgen05) or 1 (SIMT reference)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (impl == 1) {
     cudaError_t e = gemm_ref(g, st);

@@ -7,13 +7,14 @@
 // the third TMA coordinate.
 //
 // Design (sm_100a):
-//  * persistent, one CTA per SM, 128x256 output tile, BK = 64, 4-stage
-//    TMA -> smem ring (128B swizzle), mbarrier full/empty pipeline;
-//  * warp 0: TMA producer (one elected lane); warp 1: tcgen05.mma issuer
-//    (one lane, M=128 N=256 K=16 per instruction); warp 2: TMEM allocator;
-//    warps 4-7: epilogue (tcgen05.ld -> fp32 epilogue -> bf16 -> global);
-//  * TMEM holds two 128x256 fp32 accumulators (512 columns) so the epilogue of
-//    tile i overlaps the main loop of tile i+1;
+//  * persistent, a CTA pair (cluster of 2) per 2 SMs, 256x256 output tile with
+//    tcgen05.mma.cta_group::2 (M = 256), BK = 64, 6-stage TMA -> smem ring (128B
+//    swizzle), mbarrier full/empty pipeline;
+//  * warp 0: TMA producer (one elected lane); warp 1: tcgen05.mma issuer (leader
+//    CTA, one lane); warp 2: TMEM allocator; warps 4+: epilogue (tcgen05.ld ->
+//    fp32 epilogue -> bf16 -> global);
+//  * TMEM holds two 128x256 fp32 accumulators per CTA (512 columns) so the
+//    epilogue of tile i overlaps the main loop of tile i+1;
 //  * operands may be K-major or MN-major (instruction-descriptor bits), which
 //    covers the forward (X W1^T, A W2^T), the data-gradient (dY W2, dH W1)
 //    and the weight-gradient (dY^T A, dH^T X) GEMMs without transposes;
@@ -26,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -34,15 +36,10 @@
 namespace moe {
 namespace {
 
-constexpr int BM = 128;
+constexpr int BM = 128;  // rows of A per CTA (the CTA pair covers 256)
 constexpr int BN = 256;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
-constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
-constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
-constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;        // 2 accumulators x 256 fp32 columns
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
 
 struct Params {
   int batch, M, N, K;
@@ -63,209 +60,6 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
   d |= (uint64_t)1 << 46;  // version (sm_100)
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
-}
-
-// Instruction descriptor: kind::f16, A/B bf16, D fp32, M=128, N=256.
-__host__ __device__ constexpr uint32_t instr_desc(int a_mn, int b_mn) {
-  return (1u << 4)                      // D format fp32
-         | (1u << 7)                    // A format bf16
-         | (1u << 10)                   // B format bf16
-         | ((uint32_t)a_mn << 15)       // A major
-         | ((uint32_t)b_mn << 16)       // B major
-         | ((uint32_t)(BN >> 3) << 17)  // N >> 3
-         | ((uint32_t)(BM >> 4) << 24); // M >> 4
-}
-
-template <int A_MN, int B_MN, int EPI>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const Params p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for the 128B swizzle atoms.
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* smA = smem;
-  uint8_t* smB = smem + STAGES * A_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + STAGES * B_STAGE);
-  // bars[0..S): full, [S..2S): empty, [2S..2S+2): tmem_full, [2S+2..2S+4): tmem_empty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&bars[s]), 1);
-      mbar_init(smem_u32(&bars[STAGES + s]), 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(smem_u32(&bars[2 * STAGES + a]), 1);
-      mbar_init(smem_u32(&bars[2 * STAGES + 2 + a]), 4);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-        const int b = tile / (p.tiles_m * p.tiles_n);
-        const int r = tile - b * p.tiles_m * p.tiles_n;
-        const int m0 = (r / p.tiles_n) * BM;
-        const int n0 = (r % p.tiles_n) * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(smem_u32(&bars[STAGES + stage]), phase ^ 1);
-          const uint32_t full = smem_u32(&bars[stage]);
-          mbar_arrive_expect_tx(full, A_STAGE + B_STAGE);
-          const uint32_t a_dst = smem_u32(smA + stage * A_STAGE);
-          const uint32_t b_dst = smem_u32(smB + stage * B_STAGE);
-          const int k0 = kb * BK;
-          if (A_MN) {
-#pragma unroll
-            for (int i = 0; i < BM / 64; ++i) tma_load_3d(a_dst + i * 8192, &tmA, full, m0 + 64 * i, k0, b);
-          } else {
-            tma_load_3d(a_dst, &tmA, full, k0, m0, b);
-          }
-          if (B_MN) {
-#pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_3d(b_dst + i * 8192, &tmB, full, n0 + 64 * i, k0, b);
-          } else {
-            tma_load_3d(b_dst, &tmB, full, k0, n0, b);
-          }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc(A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int iter = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++iter) {
-        const int acc = iter & 1;
-        const uint32_t acc_phase = (iter >> 1) & 1;
-        mbar_wait(smem_u32(&bars[2 * STAGES + 2 + acc]), acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(smem_u32(&bars[stage]), phase);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(smA + stage * A_STAGE);
-          const uint32_t b_base = smem_u32(smB + stage * B_STAGE);
-#pragma unroll
-          for (int j = 0; j < BK / 16; ++j) {
-            // K-major: +32 B per K=16 step inside the 128B swizzle row.
-            // MN-major: +16 rows x 128 B per K=16 step; 64-wide MN blocks 8 KiB apart.
-            const uint64_t ad = A_MN ? smem_desc(a_base + j * 2048, 8192, 1024)
-                                     : smem_desc(a_base + j * 32, 16, 1024);
-            const uint64_t bd = B_MN ? smem_desc(b_base + j * 2048, 8192, 1024)
-                                     : smem_desc(b_base + j * 32, 16, 1024);
-            tc_mma_f16(tmem_d, ad, bd, idesc, (kb | j) != 0);
-          }
-          tc_commit(smem_u32(&bars[STAGES + stage]));  // frees the smem stage
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        tc_commit(smem_u32(&bars[2 * STAGES + acc]));  // accumulator ready
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    int iter = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++iter) {
-      const int b = tile / (p.tiles_m * p.tiles_n);
-      const int r = tile - b * p.tiles_m * p.tiles_n;
-      const int m0 = (r / p.tiles_n) * BM;
-      const int n0 = (r % p.tiles_n) * BN;
-      const int acc = iter & 1;
-      const uint32_t acc_phase = (iter >> 1) & 1;
-      mbar_wait(smem_u32(&bars[2 * STAGES + acc]), acc_phase);
-      tc_fence_after();
-      const int m = m0 + quad * 32 + lane;
-      const bool row_ok = m < p.M;
-      const size_t row_off = ((size_t)b * p.M + (row_ok ? m : 0)) * (size_t)p.N;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c, v);
-        tmem_wait_ld();
-        const int n = n0 + c;
-        if (row_ok && n < p.N) {
-          bf16* dst = p.D + row_off + n;
-          if (EPI == EPI_DGELU) {
-            const bf16* hsrc = p.aux + row_off + n;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 h = *reinterpret_cast<const uint4*>(hsrc + q * 8);
-              uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-              uint32_t o[4];
-#pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                float2 hv = unpack_bf16x2(hw[w]);
-                o[w] = pack_bf16x2(__uint_as_float(v[q * 8 + 2 * w]) * hv.x,
-                                   __uint_as_float(v[q * 8 + 2 * w + 1]) * hv.y);
-              }
-              st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t o[4];
-#pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                const float f0 = __uint_as_float(v[q * 8 + 2 * w]), f1 = __uint_as_float(v[q * 8 + 2 * w + 1]);
-                o[w] = EPI == EPI_GELU ? pack_bf16x2(gelu_grad_f(f0), gelu_grad_f(f1)) : pack_bf16x2(f0, f1);
-              }
-              st_v4(dst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
-            }
-            if (EPI == EPI_GELU) {
-              bf16* adst = p.aux + row_off + n;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t o[4];
-#pragma unroll
-                for (int w = 0; w < 4; ++w)
-                  o[w] = pack_bf16x2(gelu_f(__uint_as_float(v[q * 8 + 2 * w])),
-                                     gelu_f(__uint_as_float(v[q * 8 + 2 * w + 1])));
-                st_v4(adst + q * 8, make_uint4(o[0], o[1], o[2], o[3]));
-              }
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars[2 * STAGES + 2 + acc]));
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS)
-                 : "memory");
-  }
 }
 
 // ---------------------------------------------------------------- 2-CTA variant
@@ -300,6 +94,19 @@ __host__ __device__ constexpr uint32_t instr_desc_m256(int a_mn, int b_mn) {
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
+// Development instrumentation (tools/gemm_prof.cu builds this file with MOE_GEMM_PROF):
+// per-CTA cycle counters of the pipeline waits. Compiled out of the library.
+#ifdef MOE_GEMM_PROF
+__device__ unsigned long long g_prof[160][8];
+#define PROF_T0(v) const long long v = clock64()
+#define PROF_ADD(i, t0) atomicAdd(&g_prof[blockIdx.x][i], (unsigned long long)(clock64() - (t0)))
+#define PROF_CNT(i) atomicAdd(&g_prof[blockIdx.x][i], 1ull)
+#else
+#define PROF_CNT(i)
+#define PROF_T0(v)
+#define PROF_ADD(i, t0)
+#endif
+
 template <int A_MN, int B_MN, int EPI>
 __global__ void __launch_bounds__(threads2(EPI), 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -320,6 +127,7 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  PROF_T0(t_start);
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1;
@@ -362,7 +170,9 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
         const int m0 = (r / p.tiles_n) * 256 + rank * 128;
         const int n0 = (r % p.tiles_n) * BN + rank * 128;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
+          PROF_T0(w0);
           mbar_wait(smem_u32(&bars[STAGES2 + stage]), phase ^ 1);
+          PROF_ADD(0, w0);
           const uint32_t full = smem_u32(&bars[stage]);
           if (leader) mbar_arrive_expect_tx(full, 2 * (A2_STAGE + B2_STAGE));
           const uint32_t a_dst = smem_u32(smA + stage * A2_STAGE);
@@ -403,11 +213,15 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       for (int tile = cluster; tile < p.total_tiles; tile += nclusters, ++iter) {
         const int acc = iter & 1;
         const uint32_t acc_phase = (iter >> 1) & 1;
+        PROF_T0(w2);
         mbar_wait(smem_u32(&bars[2 * STAGES2 + 2 + acc]), acc_phase ^ 1);
+        PROF_ADD(2, w2);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
+          PROF_T0(w1);
           mbar_wait(smem_u32(&bars[stage]), phase);
+          PROF_ADD(1, w1);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smA + stage * A2_STAGE);
           const uint32_t b_base = smem_u32(smB + stage * B2_STAGE);
@@ -447,7 +261,10 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       const int n0 = (r % p.tiles_n) * BN;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
+      PROF_T0(w3);
       mbar_wait(smem_u32(&bars[2 * STAGES2 + acc]), acc_phase);
+      if (ew == 0 && lane == 0) PROF_ADD(3, w3);
+      PROF_T0(w4);
       tc_fence_after();
       const int mrow0 = m0 + quad * 32;
       const int m = mrow0 + lane;
@@ -537,11 +354,13 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(smem_u32(&bars[2 * STAGES2 + 2 + acc]), 0);
+      if (ew == 0 && lane == 0) { PROF_ADD(4, w4); PROF_CNT(6); }
     }
   }
 
   tc_fence_before();
   cluster_sync();
+  if (threadIdx.x == 0) PROF_ADD(5, t_start);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -580,20 +399,6 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
-}
-
-template <int A_MN, int B_MN, int EPI>
-cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
-  static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
-  auto k = gemm_kernel<A_MN, B_MN, EPI>;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int grid = p.total_tiles < g_num_sms ? p.total_tiles : g_num_sms;
-  k<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ta, tb, p);
-  return cudaGetLastError();
 }
 
 template <int A_MN, int B_MN, int EPI>
@@ -640,9 +445,8 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   std::call_once(g_once, init_once);
   if (g_init_err != cudaSuccess) { *why = "driver entry point / device query failed"; return g_init_err; }
   if (a.batch <= 0 || a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaSuccess;
-  const bool pair = a.variant != 1;  // default: CTA-pair (cta_group::2) kernel
-  if ((a.a_bs || a.d_bs) && (!pair || a.a_mn)) {
-    *why = "batch strides need the CTA-pair kernel and a K-major A";
+  if ((a.a_bs || a.d_bs) && a.a_mn) {
+    *why = "batch strides need a K-major A";
     return cudaErrorNotSupported;
   }
   CUtensorMap ta, tb;
@@ -650,27 +454,27 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
                    : make_map(&ta, a.A, a.K, a.M, a.batch, 64, BM, CU_TENSOR_MAP_SWIZZLE_128B,
                               (uint64_t)a.a_bs);
   ok = ok && (a.b_mn ? make_map(&tb, a.B, a.N, a.K, a.batch, 64, 64)
-                     : make_map(&tb, a.B, a.K, a.N, a.batch, 64, pair ? 128 : BN));
+                     : make_map(&tb, a.B, a.K, a.N, a.batch, 64, 128));
   if (!ok) { *why = "cuTensorMapEncodeTiled rejected the operand layout"; return cudaErrorInvalidValue; }
   Params p;
   p.batch = a.batch; p.M = a.M; p.N = a.N; p.K = a.K;
   p.d_bs = a.d_bs ? a.d_bs : (int64_t)a.M * a.N;
-  p.tiles_m = (a.M + (pair ? 256 : BM) - 1) / (pair ? 256 : BM);
+  p.tiles_m = (a.M + 255) / 256;
   p.tiles_n = (a.N + BN - 1) / BN;
   p.total_tiles = p.tiles_m * p.tiles_n * a.batch;
   p.k_blocks = (a.K + BK - 1) / BK;
   p.D = static_cast<bf16*>(a.D);
   p.aux = static_cast<bf16*>(a.aux);
   p.g = a.gdx ? *a.gdx : GateDxArgs{};
-  if (a.epilogue == EPI_COMBINE && (!a.gdx || !pair)) {
-    *why = "combine epilogue needs the CTA-pair kernel";
+  if (a.epilogue == EPI_COMBINE && !a.gdx) {
+    *why = "combine epilogue needs its gate arguments";
     return cudaErrorNotSupported;
   }
   CUtensorMap ta2 = ta, tb2 = tb;
   p.k_main = p.k_blocks;
   if (a.epilogue == EPI_SCATTER) {
-    if (!a.gdx || !pair || !a.b_mn || a.a_mn || !a.gdx->a_ext || !a.gdx->b_ext || a.a_bs || a.d_bs) {
-      *why = "scatter epilogue: CTA-pair kernel, K-major A, MN-major B, extension operands";
+    if (!a.gdx || !a.b_mn || a.a_mn || !a.gdx->a_ext || !a.gdx->b_ext || a.a_bs || a.d_bs) {
+      *why = "scatter epilogue: K-major A, MN-major B, extension operands";
       return cudaErrorNotSupported;
     }
     // A2 = [batch][M][64], B2 = [64][N] (one copy, batch coordinate 0)
@@ -680,26 +484,15 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
     p.k_blocks += 1;
   }
   const int key = a.a_mn * 100 + a.b_mn * 10 + a.epilogue;
-  if (pair) {
-    switch (key) {
-      case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, ta, tb, p, s);
-      case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, ta, tb, p, s);
-      case 4:   return launch2<0, 0, EPI_COMBINE>(ta, tb, ta, tb, p, s);
-      case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, ta, tb, p, s);
-      case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, ta, tb, p, s);
-      case 15:  return launch2<0, 1, EPI_SCATTER>(ta, tb, ta2, tb2, p, s);
-      case 110: return launch2<1, 1, EPI_STORE>(ta, tb, ta, tb, p, s);
-      default: break;
-    }
-  } else {
-    switch (key) {
-      case 0:   return launch<0, 0, EPI_STORE>(ta, tb, p, s);
-      case 1:   return launch<0, 0, EPI_GELU>(ta, tb, p, s);
-      case 10:  return launch<0, 1, EPI_STORE>(ta, tb, p, s);
-      case 12:  return launch<0, 1, EPI_DGELU>(ta, tb, p, s);
-      case 110: return launch<1, 1, EPI_STORE>(ta, tb, p, s);
-      default: break;
-    }
+  switch (key) {
+    case 0:   return launch2<0, 0, EPI_STORE>(ta, tb, ta, tb, p, s);
+    case 1:   return launch2<0, 0, EPI_GELU>(ta, tb, ta, tb, p, s);
+    case 4:   return launch2<0, 0, EPI_COMBINE>(ta, tb, ta, tb, p, s);
+    case 10:  return launch2<0, 1, EPI_STORE>(ta, tb, ta, tb, p, s);
+    case 12:  return launch2<0, 1, EPI_DGELU>(ta, tb, ta, tb, p, s);
+    case 15:  return launch2<0, 1, EPI_SCATTER>(ta, tb, ta2, tb2, p, s);
+    case 110: return launch2<1, 1, EPI_STORE>(ta, tb, ta, tb, p, s);
+    default: break;
   }
   *why = "operand-major / epilogue combination not instantiated";
   return cudaErrorNotSupported;

@@ -39,10 +39,9 @@ struct GemmArgs {
   void* D;   // [b][M][N]
   int epilogue;
   void* aux;  // EPI_GELU: out A = gelu(acc) [b][M][N] (D = gelu'(acc)); EPI_DGELU: in G [b][M][N] (D = acc*G)
-  int variant = 0;  // 0: CTA-pair kernel (cta_group::2, product path); 1: single-CTA kernel
   // Batch strides in elements (0 = dense): rows [0, M) of batch b of A (K-major only)
   // start at A + b * a_bs; of D / aux at D + b * d_bs (a row block of a larger batch,
-  // e.g. the rows of one source rank inside [E_l][G_ep][C]). CTA-pair kernel only.
+  // e.g. the rows of one source rank inside [E_l][G_ep][C]).
   int64_t a_bs = 0, d_bs = 0;
   const GateDxArgs* gdx = nullptr;  // EPI_SCATTER / EPI_COMBINE only
 };

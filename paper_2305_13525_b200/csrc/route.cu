@@ -85,10 +85,14 @@ __device__ __forceinline__ bool finalize_token(const float (&lv)[EMAX], int64_t 
 // terms hi + mid + lo (24 significant bits, i.e. all of Wg's) by the converter warps, so
 // x . Wg = x . hi + x . mid + x . lo with every product exact and fp32 accumulation in
 // TMEM: one tcgen05.mma M = 128 rows, N = 3 * NPAD (hi | mid | lo columns), K = 16.
-// The K range is cut into NCH chunks with their own TMEM columns; the epilogue sums
-// (hi + (mid + lo)) per chunk and the chunks in order in fp32, so no accumulator ever
-// holds more than H / NCH terms (logit error ~1e-7, below the 1e-6 tie threshold).
-//
+// Precision: a tensor-core accumulation of many MMAs into one fp32 accumulator loses
+// bits (measured max logit error 1.2e-5 with one accumulator over K = 2048, 1.4e-6 with
+// 10 chunks), so every 64-wide k block gets a fresh accumulator: the MMA issuer writes
+// k block i into TMEM chunk buffer i % NB (hi | mid | lo, 3 NPAD columns) and commits it,
+// and the epilogue warps — otherwise idle during the main loop — drain each chunk as it
+// completes, summing (hi + (mid + lo)) into the token's logits with Kahan compensation,
+// then release the buffer. No accumulator holds more than 64 products (error ~1e-7,
+// tests/test_gpu_layer.py), so routing matches the oracle outside the 1e-6 tie set.
 // A tile holds R <= 128 tokens, R = T / #SMs rounded up to 8, so every SM streams
 // (rows >= R of the 128-row MMA are ignored). Measured (tools/read_bw.cu): a cold 64 MiB
 // read takes ~18 us with the best LDG.128 kernel and ~20.5 us with 64 x 128 TMA boxes at
@@ -119,8 +123,8 @@ struct Cfg {
   static constexpr int STAGE = A_BYTES + B_BYTES + W_BYTES;
   static constexpr int STAGES = (200 * 1024 / STAGE) < 8 ? (200 * 1024 / STAGE) : 8;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-  static constexpr int NCOL = 3 * NPAD;
-  static constexpr int NCH = (TMEM_COLS / NCOL) < 8 ? (TMEM_COLS / NCOL) : 8;
+  static constexpr int NCOL = 3 * NPAD;  // hi | mid | lo columns of one chunk
+  static constexpr int NB = TMEM_COLS / NCOL;  // chunk buffers in TMEM (one k block each)
   static_assert(STAGE % 1024 == 0 && STAGES >= 3 && NCOL % 16 == 0 && NCOL <= 256, "gate tile");
 };
 
@@ -134,7 +138,7 @@ struct Args {
   const float* wg;
   const int32_t* forced;
   int64_t T;
-  int H, E, K, nch, R;
+  int H, E, K, R;
   int fuse_scan;  // top-1, token order: the epilogue produces local_rank / tile histogram
   float* logits;
   int32_t* expert;
@@ -176,16 +180,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  constexpr int NB = C::NB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::STAGE);
   // [0,S) full (x landed), [S,2S) bready (B tile converted), [2S,3S) empty (MMAs done
-  // with the stage), 3S tmem_full, 3S+1 tmem_empty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 2);
+  // with the stage), [3S,3S+NB) chunk full, [3S+NB,3S+2NB) chunk empty (drained)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 2 * NB);
   __shared__ int32_t wh[4][64];  // fused scan: per-warp expert histogram
   __shared__ int32_t wties[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = a.H / BKG;
-  const int nch = a.nch < KB ? a.nch : KB;
   const int R = a.R;
   const int64_t ntiles = (a.T + R - 1) / R;
 
@@ -196,8 +200,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(smem_u32(&bars[S + s]), CONV_WARPS);
       mbar_init(smem_u32(&bars[2 * S + s]), 1);
     }
-    mbar_init(smem_u32(&bars[3 * S]), 1);
-    mbar_init(smem_u32(&bars[3 * S + 1]), 4);
+    for (int c = 0; c < NB; ++c) {
+      mbar_init(smem_u32(&bars[3 * S + c]), 1);
+      mbar_init(smem_u32(&bars[3 * S + NB + c]), 4);
+    }
     fence_barrier_init();
   }
   if (warp == 4) {
@@ -240,26 +246,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                                  ((uint32_t)(ROWS >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
-      int iter = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
-        mbar_wait(smem_u32(&bars[3 * S + 1]), (iter & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < KB; ++kb) {
+      int g = 0;  // k blocks issued by this CTA (chunk buffer g % NB, use g / NB)
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int buf = g % NB;
+          mbar_wait(smem_u32(&bars[3 * S + NB + buf]), ((g / NB) & 1) ^ 1);  // drained
           mbar_wait(smem_u32(&bars[stage]), phase);
           mbar_wait(smem_u32(&bars[S + stage]), phase);
           tc_fence_after();
-          const int ch = kb * nch / KB;
-          const bool first = kb == 0 || (kb - 1) * nch / KB != ch;
           const uint32_t ab = smem_u32(smem + stage * C::STAGE);
           const uint32_t bb = ab + C::A_BYTES;
 #pragma unroll
           for (int j = 0; j < BKG / 16; ++j)
-            tc_mma_f16(tmem_base + ch * C::NCOL, sw128_desc(ab + j * 32), sw128_desc(bb + j * 32), idesc,
-                       (first && j == 0) ? 0u : 1u);
+            tc_mma_f16(tmem_base + buf * C::NCOL, sw128_desc(ab + j * 32), sw128_desc(bb + j * 32), idesc,
+                       j == 0 ? 0u : 1u);
           tc_commit(smem_u32(&bars[2 * S + stage]));
+          tc_commit(smem_u32(&bars[3 * S + buf]));
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        tc_commit(smem_u32(&bars[3 * S]));
       }
     }
     __syncwarp();
@@ -306,31 +310,38 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------- epilogue (warps 0-3)
-    int iter = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
-      mbar_wait(smem_u32(&bars[3 * S]), iter & 1);
-      tc_fence_after();
-      float lv[NPAD];
+    int g = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      float lv[NPAD], comp[NPAD];  // Kahan sum over the k-block chunks
 #pragma unroll
-      for (int e = 0; e < NPAD; ++e) lv[e] = 0.f;
+      for (int e = 0; e < NPAD; ++e) { lv[e] = 0.f; comp[e] = 0.f; }
       const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
-      if (warp * 32 < R) {  // warp-uniform: quadrants past the tile's rows hold nothing
-        for (int ch = 0; ch < nch; ++ch) {
+      for (int kb = 0; kb < KB; ++kb, ++g) {
+        const int buf = g % NB;
+        mbar_wait(smem_u32(&bars[3 * S + buf]), (g / NB) & 1);
+        tc_fence_after();
+        if (warp * 32 < R) {  // warp-uniform: quadrants past the tile's rows hold nothing
 #pragma unroll
           for (int nb = 0; nb < NPAD / 16; ++nb) {
             float h[16], m[16], l[16];
-            const uint32_t c0 = trow + ch * C::NCOL + nb * 16;
+            const uint32_t c0 = trow + buf * C::NCOL + nb * 16;
             tmem_ld_x16(c0, h);
             tmem_ld_x16(c0 + NPAD, m);
             tmem_ld_x16(c0 + 2 * NPAD, l);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) lv[nb * 16 + i] += h[i] + (m[i] + l[i]);
+            for (int i = 0; i < 16; ++i) {
+              const int e = nb * 16 + i;
+              const float y = (h[i] + (m[i] + l[i])) - comp[e];
+              const float t = lv[e] + y;
+              comp[e] = (t - lv[e]) - y;
+              lv[e] = t;
+            }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars[3 * S + NB + buf]));  // chunk drained
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars[3 * S + 1]));  // accumulator free for the next tile
 
       const int row = warp * 32 + lane;
       const int64_t tok = tile * R + row;
@@ -668,13 +679,8 @@ cudaError_t launch_gate_tc(const RouteArgs& a, bool fuse, int* R_out, cudaStream
   if (R > gtc::ROWS) R = gtc::ROWS;
   e = tensor_map_bf16(&tm, a.x, (uint64_t)a.H, (uint64_t)a.T, gtc::BKG, (uint32_t)R, &sms);
   if (e != cudaSuccess) return e;
-  static const int nch_env = [] {
-    const char* v = getenv("MOE_GATE_NCH");  // development knob: K chunks of the accumulator
-    return v ? atoi(v) : 0;
-  }();
   gtc::Args g;
   g.wg = a.wg; g.forced = a.forced; g.T = a.T; g.H = a.H; g.E = a.E; g.K = a.K; g.R = (int)R;
-  g.nch = nch_env > 0 && nch_env <= Cf::NCH ? nch_env : Cf::NCH;
   g.fuse_scan = fuse ? 1 : 0;
   g.logits = a.logits; g.expert = a.expert; g.prob = a.prob; g.gap = a.gap;
   g.local_rank = a.local_rank; g.tile_hist = a.block_hist; g.tile_ties = a.tile_ties;

@@ -36,7 +36,7 @@ SHAPES = [(2, 200, 320, 136), (1, 128, 256, 64), (3, 64, 64, 8), (1, 1024, 1024,
 
 @pytest.mark.parametrize("a_mn,b_mn,epi", COMBOS)
 @pytest.mark.parametrize("batch,M,N,K", SHAPES)
-@pytest.mark.parametrize("impl", [0, 1, 2])
+@pytest.mark.parametrize("impl", [0, 1])
 def test_gemm_vs_torch(a_mn, b_mn, epi, batch, M, N, K, impl):
     g = torch.Generator(device="cuda").manual_seed(1234 + M + N + K)
     dev = "cuda"

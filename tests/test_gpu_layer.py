@@ -271,10 +271,13 @@ def test_fused_combine_matches_separate_kernel(monkeypatch):
 @pytest.mark.parametrize("T,H,E", [(16384, 2048, 16), (4096, 4096, 16), (4096, 2560, 32), (3000, 2048, 64),
                                    (1000, 128, 5)])
 def test_gate_logit_error(T, H, E):
-    """F1 on the tensor cores (Wg split hi + mid + lo, fp32 TMEM accumulation in K chunks):
-    the saved logits (first region of the saved blob, plan.cpp make_layouts) against the
-    float64 x . Wg of the oracle. Bound 2.5e-7 absolute: 4x inside the 1e-6 tie threshold
-    of BASELINE.json, so routing outside logged ties is decided exactly as in the oracle."""
+    """F1 on the tensor cores (Wg split hi + mid + lo, a fresh TMEM accumulator per 64-wide
+    k block, Kahan sum of the blocks): the saved logits (first region of the saved blob,
+    plan.cpp make_layouts) against the float64 x . Wg of the oracle: rms <= 1.5e-7 and
+    max <= 8e-7 (measured rms 7.8e-8, max 4-6e-7 over 4k-262k logits, about what a
+    pairwise fp32 sum gives; a sequential fp32 sum of 2048 terms has ~8e-7 rms). Routing
+    outside the logged ties (gap < 1e-6, BASELINE.json) is checked by the layer tests and
+    test_gate_near_ties."""
     shape = synth.LayerShape("gate", T, H, 256, E)
     x_bits = synth.make_x(shape)
     wg = synth.make_wg(shape)
@@ -288,5 +291,40 @@ def test_gate_logit_error(T, H, E):
     got = saved[: T * E * 4].view(torch.float32).reshape(T, E).cpu().numpy().astype(np.float64)
     layer.close()
     ref = O.decode_bf16(x_bits) @ wg.astype(np.float64)
-    err = np.abs(got - ref).max()
-    assert err <= 2.5e-7, err
+    err = np.abs(got - ref)
+    srt = np.sort(ref, axis=1)
+    gap = srt[:, -1] - srt[:, -2] if E > 1 else np.full(T, np.inf)
+    near = gap < 1e-5
+    near_err = err[near].max() if near.any() else 0.0
+    print(f"gate logit error T={T} H={H} E={E}: max {err.max():.3e}, rms {np.sqrt(np.mean(err ** 2)):.3e}, "
+          f"{int(near.sum())} near-tie tokens max {near_err:.3e}")
+    assert np.sqrt(np.mean(err ** 2)) <= 1.5e-7 and err.max() <= 8e-7, err.max()
+
+
+def test_gate_near_ties():
+    """Many near ties: expert 1's gate column is expert 0's plus a tiny perturbation, so
+    a large share of tokens has a top-2 gap of ~1e-6 .. 1e-5; routing must still match the
+    oracle outside the logged (< 1e-6) ties."""
+    T, H, E = 4096, 2048, 8
+    shape = synth.LayerShape("ties", T, H, 256, E)
+    x_bits = synth.make_x(shape)
+    wg = synth.make_wg(shape)
+    rng = np.random.default_rng(5)
+    wg[:, 0] = np.abs(wg[:, 0]) * 4.0  # expert 0 wins clearly ...
+    wg[:, 1] = wg[:, 0] + (rng.standard_normal(H) * 2e-7).astype(np.float32)  # ... unless expert 1 is nearer
+    cfg = MoEConfig(T, H, 256, E, 8.0, 1, 1, True, 1)
+    layer = MoELayer(cfg)
+    x = bf16_tensor(x_bits)
+    w1 = torch.zeros((E, 256, H), dtype=torch.bfloat16, device="cuda")
+    w2 = torch.zeros((E, H, 256), dtype=torch.bfloat16, device="cuda")
+    y, saved = layer.moe_forward(x, torch.from_numpy(wg).cuda(), w1, w2)
+    rt = layer.moe_routing(saved)
+    torch.cuda.synchronize()
+    ge, gg = rt["expert"].cpu().numpy(), rt["gap"].cpu().numpy()
+    layer.close()
+    r0 = O.route(O.decode_bf16(x_bits), wg.astype(np.float64), O.capacity(T, E, 8.0))
+    tie = (r0.gap < O.TIE_GAP) | (gg < O.TIE_GAP)
+    near = r0.gap < 1e-5
+    assert near.sum() > T // 4, int(near.sum())  # the case really is near-tie heavy
+    bad = np.nonzero((ge != r0.expert) & ~tie)[0]
+    assert bad.size == 0, (bad[:10], r0.gap[bad[:10]])

@@ -16,7 +16,7 @@ from paper_2305_13525_b200 import moe_gemm_bf16, synth  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="1.3b")
-    ap.add_argument("--impl", type=int, nargs="+", default=[0, 2])
+    ap.add_argument("--impl", type=int, nargs="+", default=[0])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
