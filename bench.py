@@ -396,9 +396,10 @@ def main():
     gemm_ms = st["kernel_ms"]["gemm"] / args.steps
     peaks, peak_src = load_peaks()
     achieved = gemm_flops_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
-    # frac against the measured burst peak (conservative, the same in every line); the
-    # sustained figure (the GEMMs run inside a long step) is reported beside it
-    peak = peaks["bf16_tflops"]
+    # the GEMMs are timed inside a long step (back-to-back launches under the power cap), so
+    # the denominator is the measured SUSTAINED bf16 figure (the contract's rule for a kernel
+    # timed inside a long step); the burst fraction is reported beside it, the same in every line
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
@@ -411,10 +412,10 @@ def main():
     gemm_launch_ms = gemm_ms / 6.0
     roofline = {"bound": "tensor", "kernel": "gemm2_kernel (tcgen05 cta_group::2, 6 launches/step)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "peak_kind": f"{peak_src} bf16 burst",
-                "peak_sustained": peaks.get("bf16_tflops_sustained"),
+                "peak_kind": f"{peak_src} bf16 sustained (GEMMs timed inside the step)",
+                "peak_burst": peaks["bf16_tflops"],
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "frac_of_sustained": (achieved / peaks.get('bf16_tflops_sustained', peak)) if achieved else None,
+                "frac_of_burst": (achieved / peaks["bf16_tflops"]) if achieved else None,
                 "algorithmic_flop_per_launch": gemm_flops_step / 6.0,
                 # padded: every capacity slot computed (empty slots included), SURVEY §8(d)
                 "padded_tflops": (12.0 * H * Fl * El * L["rows_per_expert"]) / (gemm_ms / 1e3) / 1e12

@@ -4,8 +4,8 @@
 //   dWg   = sum_t x_t^T dl_t                                     (deterministic split-K)
 // dl and Wg are fp32; each is split into bf16 hi + lo so the products carry ~16
 // mantissa bits (relative error ~2^-17 per term, far inside the 1e-2 gradient
-// tolerance); x is exact bf16. Routing-critical arithmetic (the forward gate) stays
-// on fp32 CUDA cores in route.cu.
+// tolerance); x is exact bf16. (The forward gate's contraction, which decides the
+// routing, uses a three-term split of Wg instead: route.cu.)
 #include <atomic>
 #include <cstdlib>
 #include <cuda.h>
