@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--config", default=None, choices=[None, "1.3b", "2.7b", "6.7b"])
     p.add_argument("--vanilla", action="store_true", help="disable DTD (G_tensor > 1 configs)")
     p.add_argument("--gt", type=int, default=None, help="G_tensor override (BASELINE scaling sweep)")
+    p.add_argument("--nvls", action="store_true", help="DTD all-gathers on NVLink SHARP multicast (MOE_F_NVLS)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-optim", action="store_true", help="skip the tiled-optimizer measurement")
@@ -307,7 +308,7 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, world, rank)
 
-    from paper_2305_13525_b200 import MOE_F_STATS, MOE_F_TIMING, MoEConfig, MoELayer, lib
+    from paper_2305_13525_b200 import MOE_F_NVLS, MOE_F_STATS, MOE_F_TIMING, MoEConfig, MoELayer, lib
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -319,7 +320,7 @@ def main():
 
     name, T, H, F, E, gt, gep = workload(args, world)
     dtd = not args.vanilla
-    cfg = MoEConfig(T, H, F, E, 1.0, gt, gep, dtd, MOE_F_STATS | MOE_F_TIMING)
+    cfg = MoEConfig(T, H, F, E, 1.0, gt, gep, dtd, MOE_F_STATS | MOE_F_TIMING | (MOE_F_NVLS if args.nvls else 0))
     layer = MoELayer(cfg, world, rank, dev)
     L = layer.layout
     El, Fl = L["experts_local"], L["ffn_local"]
@@ -543,7 +544,7 @@ def main():
                "data": "synthetic (x, dy ~ N(0,1); Wg ~ N(0,1/H); W1 ~ N(0,1/H); W2 ~ N(0,1/F))",
                "config": {"workload": name, "tokens_per_group": T, "hidden": H, "ffn": F, "experts": E,
                           "capacity_factor": 1.0, "g_tensor": gt, "g_expert": gep,
-                          "dtd": bool(dtd and gt > 1), "token_groups": S,
+                          "dtd": bool(dtd and gt > 1), "nvls": bool(args.nvls and dtd and gt > 1), "token_groups": S,
                           "l2": "no flush: >1 GB expert weights + activations per step exceed 126 MB L2"},
                "roofline": roofline, "hbm_steps": hbm, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(round(launches_per_step * args.steps)),

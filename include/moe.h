@@ -78,6 +78,18 @@ typedef enum {
                                      issues no collectives (Communication-aware Activation
                                      Checkpointing); without it the replay
                                      re-runs the forward's collectives (plain checkpointing) */
+#define MOE_F_NVLS 256u           /* DTD (g_tensor > 1, peer exchange) with the all-gathers on
+                                     NVLink SHARP multicast: each
+                                     rank sends its own slot slice to the same-t rank of the
+                                     destination EP group (the a2a of 1/G_t of the tokens,
+                                     PAPER.md:1153-1155) and then stores the slice it received
+                                     once through its TP group's multicast mapping
+                                     (multimem.st; the switch replicates it to every TP rank,
+                                     PAPER.md:1155-1158) instead of writing G_t copies itself;
+                                     same on the return and backward exchanges. Needs
+                                     multicast-capable GPUs (MOE_ERR_UNSUPPORTED otherwise);
+                                     emulated groups run the same data flow with unicast
+                                     stores. Ignored without DTD in effect.                  */
 /* Gating variants (the paper cites the gate's lineage,
  * PAPER.md:96-97, without defining it): */
 #define MOE_F_RANDOM_PRIORITY 64u /* random token selection (R20): capacity slots

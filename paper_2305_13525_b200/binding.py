@@ -24,6 +24,7 @@ MOE_F_CHECKPOINT = 16
 MOE_F_CAC = 32
 MOE_F_RANDOM_PRIORITY = 64
 MOE_F_AUX_LOSS = 128
+MOE_F_NVLS = 256
 KERNEL_CLASSES = ("route", "dispatch", "gemm", "combine", "combine_bwd", "gate_bwd", "comm", "xfer")
 COLL_NAMES = ("a2a", "allgather", "reducescatter", "allreduce")
 

@@ -16,7 +16,7 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmoe.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["gemm_sm100.cu", "route.cu", "permute.cu", "gate_bwd.cu", "peer.cu", "optim.cu", "plan.cpp", "comm.cpp", "api.cpp"]
+SOURCES = ["gemm_sm100.cu", "route.cu", "permute.cu", "gate_bwd.cu", "peer.cu", "optim.cu", "plan.cpp", "comm.cpp", "nvls.cpp", "api.cpp"]
 
 
 def nccl_dirs() -> tuple[str, str]:

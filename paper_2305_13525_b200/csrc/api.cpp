@@ -364,7 +364,7 @@ PeerDst peer_dst(const moe_ctx* c, int win) {
   pd.nwin = c->comm->nwin;
   pd.win = win;
   pd.d = d.d; pd.ep = d.ep; pd.t = d.t; pd.Gt = d.Gt; pd.Gep = d.Gep; pd.El = d.El;
-  pd.dtd = d.dtd ? 1 : 0;
+  pd.dtd = d.dtd && !d.nvls ? 1 : 0;  // folded all-gather: write every TP rank of the destination
   return pd;
 }
 
@@ -479,6 +479,38 @@ moe_status barrier(moe_ctx* c, cudaStream_t st) {
   return MOE_OK;
 }
 
+// MOE_F_NVLS: DTD's all-gather as its own step — this rank's slice of window `win`
+// (expert space [E_l][G_t][G_ep][C_s][H] or slot space [G_t][E][C_s][H]) goes once through
+// the TP group's multicast mapping (emulated ranks: a store per TP peer), then a barrier.
+moe_status nvls_allgather(moe_ctx* c, int win, bool expert_space, int pass, cudaStream_t st) {
+  const Dims& d = c->d;
+  moe_comm* m = c->comm;
+  TpAllGather ag;
+  ag.table = m->d_table;
+  ag.nwin = m->nwin;
+  ag.win = win;
+  ag.rank = d.rank;
+  ag.tp0 = d.rank - d.t;
+  ag.Gt = d.Gt;
+  ag.mc = m->mcwin.empty() ? nullptr : m->mcwin[win];
+  const uint64_t row = (uint64_t)d.H * 2;
+  if (expert_space) {
+    ag.seg_bytes = (uint64_t)d.Gep * d.Cs * row;
+    ag.stride = (uint64_t)d.Gt * ag.seg_bytes;
+    ag.nseg = d.El;
+  } else {
+    ag.seg_bytes = (uint64_t)d.E * d.Cs * row;
+    ag.stride = 0;
+    ag.nseg = 1;
+  }
+  ag.base_off = (uint64_t)d.t * ag.seg_bytes;
+  CUDA_TRY(c, tp_allgather(ag, st));  // timed inside the caller's comm scope
+  c->stats.kernel_launches[MOE_K_COMM] += 1;
+  TRY0(barrier(c, st));
+  ledger(c, MOE_COLL_ALLGATHER, pass, (int64_t)(ag.seg_bytes * ag.nseg));  // egress: the slice, once
+  return MOE_OK;
+}
+
 moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_t st) {
   const Dims& d = c->d;
   TRY0(barrier(c, st));
@@ -490,6 +522,7 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
   rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E; rr.H = d.H;
   rr.Cs = d.Cs;
   rr.dtd = d.dtd ? 1 : 0;
+  rr.fold = d.dtd && !d.nvls ? 1 : 0;
   CUDA_TRY(c, reduce_return(rr, st));
   c->stats.kernel_launches[MOE_K_COMM] += 1;
   TRY0(barrier(c, st));
@@ -497,7 +530,8 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
   if (d.dtd) ledger(c, MOE_COLL_REDUCESCATTER, pass, xe * (d.Gt - 1) / d.Gt);
   else ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * xe * (d.Gt - 1) / d.Gt);
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
-  if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
+  if (d.nvls) TRY0(nvls_allgather(c, dst_win, false, pass, st));
+  else if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
   return MOE_OK;
 }
 
@@ -507,7 +541,7 @@ moe_status publish(moe_ctx* c, bool dispatch, int pass, cudaStream_t st) {
   TRY0(barrier(c, st));
   const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
-  if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);
+  if (d.dtd && !d.nvls) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);  // NVLS: nvls_allgather
   return MOE_OK;
 }
 
@@ -563,6 +597,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, pass, st));
+    if (d.nvls) TRY(nvls_allgather(c, c->comm->wx(rslot), true, pass, st));
   } else {
     Scope sc_(c, MOE_K_DISPATCH, st, 1);
     CUDA_TRY(c, dispatch(x, tok_of, count, ss, lo, hi, D, at<int32_t>(saved, sv.slot), d.T,
@@ -1040,6 +1075,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, 1, st));
+    if (d.nvls) TRY(nvls_allgather(c, moe_comm::W_DY, true, 1, st));
   } else if (fused_dx) {
     // B1 + the head of B10 in one launch (dl, extension operands, dropped rows)
     Scope sc_(c, MOE_K_COMBINE_BWD, st, 1);
@@ -1095,6 +1131,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       rr.dst_win = moe_comm::W_DS;
       rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E;
       rr.H = d.H; rr.Cs = d.Cs; rr.dtd = d.dtd ? 1 : 0;
+      rr.fold = d.dtd && !d.nvls ? 1 : 0;
       CUDA_TRY(c, reduce_return(rr, st));
       c->stats.kernel_launches[MOE_K_COMM] += 1;
     }
@@ -1106,7 +1143,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     if (d.dtd) ledger(c, MOE_COLL_REDUCESCATTER, 1, xe * (d.Gt - 1) / d.Gt);
     else ledger(c, MOE_COLL_ALLREDUCE, 1, 2 * xe * (d.Gt - 1) / d.Gt);
     if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
-    if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
+    if (d.nvls) TRY(nvls_allgather(c, moe_comm::W_DS, false, 1, st));
+    else if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
   } else if (d.peer) {
     // B7-B9 (TP reduction + return pieces) on the side stream, overlapping the
     // weight-gradient GEMMs, which do not feed them

@@ -2,6 +2,8 @@
 #include "comm.h"
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
@@ -88,6 +90,7 @@ moe_status make_comm_plan(const moe_config* cfgs, int n, int world, int rank, Co
     }
     q.peer |= d.peer;
     q.nccl |= world > 1 && !d.peer;
+    q.nvls |= d.nvls;
     q.expert_space = std::max(q.expert_space, (size_t)d.El * d.R * d.H * 2);
     q.slot_space = std::max(q.slot_space, (size_t)d.E * d.C * d.H * 2);
     if (d.Gt > 1) q.tp_space = std::max(q.tp_space, (size_t)d.El * d.R * d.H * 2);
@@ -136,6 +139,7 @@ moe_status comm_create(const moe_config* cfgs, int n, const uint8_t* uid, moe_em
     cudaError_t _e = (expr);                                       \
     if (_e != cudaSuccess) return bail(cuda_fail(_e, #expr, why)); \
   } while (0)
+  size_t region = 0;  // bytes of the NVLS multicast region (MOE_F_NVLS over IPC)
   CB(cudaHostAlloc(reinterpret_cast<void**>(&m->err_host), sizeof(int32_t), cudaHostAllocMapped));
   *m->err_host = 0;
   CB(cudaHostGetDevicePointer(reinterpret_cast<void**>(&m->err_dev), m->err_host, 0));
@@ -153,8 +157,20 @@ moe_status comm_create(const moe_config* cfgs, int n, const uint8_t* uid, moe_em
       sz[m->wx(r)] = plan.expert_space;
       sz[m->wo(r)] = plan.slot_space;
     }
+    // MOE_F_NVLS over IPC: the X / O rings, dY and dS live in the multicast region (created
+    // once the world communicator exists, below); everything else is cudaMalloc'd
+    m->mcwin.assign(m->nwin, nullptr);
+    m->region_off.assign(m->nwin, SIZE_MAX);
+    if (plan.nvls && !emu && world > 1) {
+      for (int w = 0; w < m->nwin; ++w) {
+        const bool in = w == moe_comm::W_DY || w == moe_comm::W_DS || w >= moe_comm::W_RING;
+        if (!in || !sz[w]) continue;
+        m->region_off[w] = region;
+        region += round_gran(sz[w]);
+      }
+    }
     for (int w = 0; w < m->nwin; ++w) {
-      if (!sz[w]) continue;
+      if (!sz[w] || m->region_off[w] != SIZE_MAX) continue;
       CB(cudaMalloc(&m->win[w], round_gran(sz[w])));
       CB(cudaMemset(m->win[w], 0, round_gran(sz[w])));
     }
@@ -183,13 +199,22 @@ moe_status comm_create(const moe_config* cfgs, int n, const uint8_t* uid, moe_em
       m->world_comm = nullptr;
       return bail(MOE_ERR_NCCL);
     }
+    if (region) {
+      s = nvls_create(&m->nvls, region, world, rank, plan.Gt, m->world_comm, why);
+      if (s != MOE_OK) return bail(s);
+      for (int w = 0; w < m->nwin; ++w)
+        if (m->region_off[w] != SIZE_MAX) {
+          m->win[w] = static_cast<uint8_t*>(m->nvls.uc) + m->region_off[w];
+          m->mcwin[w] = static_cast<uint8_t*>(m->nvls.mcva) + m->region_off[w];
+        }
+    }
     if (plan.peer) {
       // exchange the IPC handles of every window once over the world communicator
       const int nw = m->nwin;
       std::vector<cudaIpcMemHandle_t> mine(nw);
       std::memset(mine.data(), 0, sizeof(cudaIpcMemHandle_t) * nw);
       for (int w = 0; w < nw; ++w)
-        if (m->win[w]) CB(cudaIpcGetMemHandle(&mine[w], m->win[w]));
+        if (m->win[w] && m->region_off[w] == SIZE_MAX) CB(cudaIpcGetMemHandle(&mine[w], m->win[w]));
       const size_t hb = sizeof(cudaIpcMemHandle_t) * nw;
       uint8_t* dbuf = nullptr;
       CB(cudaMalloc(&dbuf, hb * world));
@@ -210,6 +235,10 @@ moe_status comm_create(const moe_config* cfgs, int n, const uint8_t* uid, moe_em
           void*& slot = m->h_table[(size_t)q * nw + w];
           if (q == rank) { slot = m->win[w]; continue; }
           if (!m->win[w]) continue;  // same plan on every rank: absent everywhere
+          if (m->region_off[w] != SIZE_MAX) {  // NVLS region: the peer's fabric-handle mapping
+            slot = static_cast<uint8_t*>(m->nvls.peer_uc[q]) + m->region_off[w];
+            continue;
+          }
           CB(cudaIpcOpenMemHandle(&slot, all[(size_t)q * nw + w], cudaIpcMemLazyEnablePeerAccess));
           m->opened.push_back(slot);
         }
@@ -240,8 +269,12 @@ void comm_destroy(moe_comm* m) {
   if (!m) return;
   if (m->tr == TR_EMU && m->emu) host_barrier(m->emu, 10000, BAR_DESTROY);  // no rank frees while a peer may write
   for (void* p : m->opened) cudaIpcCloseMemHandle(p);
-  for (void* p : m->win)
-    if (p) cudaFree(p);
+  for (size_t w = 0; w < m->win.size(); ++w)
+    if (m->win[w] && (m->region_off.empty() || m->region_off[w] == SIZE_MAX)) cudaFree(m->win[w]);
+  if (m->nvls.size) {
+    cudaDeviceSynchronize();  // no exchange may still be writing the region
+    nvls_destroy(&m->nvls);
+  }
   if (m->meta) cudaFree(m->meta);
   if (m->err_host) cudaFreeHost(m->err_host);
   if (m->tp_comm) ncclCommDestroy(m->tp_comm);

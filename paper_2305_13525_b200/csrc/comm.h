@@ -17,6 +17,7 @@
 //         communicator carry the collectives (the library baseline).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -40,6 +41,7 @@ struct CommPlan {
   int64_t timeout_ms = 60000;    // deadline of every barrier / signal wait
   bool peer = false;             // any config uses the peer-memory exchange
   bool nccl = false;             // any config uses MOE_F_NCCL_EXCHANGE
+  bool nvls = false;             // any config uses MOE_F_NVLS (multicast region)
   size_t expert_space = 0, slot_space = 0, tp_space = 0;
   size_t flags_bytes = 0, meta_bytes = 0;
   size_t total = 0;              // device bytes moe_comm_create allocates
@@ -47,6 +49,25 @@ struct CommPlan {
 
 moe_status make_comm_plan(const moe_config* cfgs, int n, int world, int rank, CommPlan* p,
                           std::string* why);
+
+// MOE_F_NVLS (nvls.cpp): the windows DTD's all-gathers write (X / O rings, dY, dS) live in one
+// VMM region per rank, mapped by every peer (fabric handles) and bound to the TP group's
+// multicast object, mapped at mcva: a multimem.st at mcva + off reaches off in every TP
+// member's region.
+struct NvlsRegion {
+  size_t size = 0;
+  int dev = 0;
+  CUmemGenericAllocationHandle phys = 0, mc = 0;
+  bool have_phys = false, have_mc = false, bound = false;
+  int own_fds[2] = {-1, -1};   // exported descriptors, closed once every peer imported them
+  void* uc = nullptr;     // this rank's region
+  void* mcva = nullptr;   // the TP group's multicast mapping
+  std::vector<void*> peer_uc;  // [world] every rank's region, mapped here
+  std::vector<CUmemGenericAllocationHandle> imported;
+};
+moe_status nvls_create(NvlsRegion* r, size_t bytes, int world, int rank, int Gt, ncclComm_t comm,
+                       std::string* why);
+void nvls_destroy(NvlsRegion* r);
 
 constexpr int SIG_OFF = 4096;    // byte offset of the signal slots in the flag window
 constexpr int PIECE_ARENA = 1 << 16;  // Piece entries in the comm's metadata block
@@ -64,6 +85,9 @@ struct moe_comm {
   int wx(int s) const { return W_RING + s; }
   int wo(int s) const { return W_RING + plan.depth + s; }
   std::vector<void*> win;        // this rank's windows [nwin]
+  std::vector<void*> mcwin;      // [nwin] multicast mapping of a window (MOE_F_NVLS, IPC), else null
+  std::vector<size_t> region_off;  // [nwin] offset in the NVLS region, or SIZE_MAX
+  moe::NvlsRegion nvls;
   std::vector<void*> opened;     // IPC mappings of the peers' windows
   std::vector<void*> h_table;    // [world][nwin]
   void** d_table = nullptr;      // device copy of h_table (in meta)

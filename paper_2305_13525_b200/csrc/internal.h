@@ -156,9 +156,22 @@ struct ReduceReturn {
   int nwin, src_win, dst_win;
   int d, ep, t, Gt, Gep, El, E, H;
   int64_t Cs;
-  int dtd;
+  int dtd;   // reduce only the rank's own slot slice
+  int fold;  // and store it to every TP rank of the source (folded all-gather), else to the same t
 };
 cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s);
+// (peer.cu) DTD all-gather in the TP group over NVLink SHARP multicast (MOE_F_NVLS):
+// segments [base_off + i * stride, + seg_bytes), i < nseg, of window `win` of this rank are
+// stored once through the group's multicast mapping `mc` (or, when null — emulated ranks —
+// to each TP peer's window) at the same offsets. seg_bytes % 16 == 0.
+struct TpAllGather {
+  void* const* table;  // device [world][nwin]
+  int nwin, win, rank, tp0, Gt;
+  void* mc;            // multicast address of window `win`, or null
+  uint64_t base_off, stride, seg_bytes;
+  int nseg;
+};
+cudaError_t tp_allgather(const TpAllGather& ag, cudaStream_t s);
 // (peer.cu) one-sided readiness flag: store `epoch` to flag (a peer's flag slot) after the
 // stream's prior work; wait until *flag >= epoch (wrap-safe). Waits are bounded: after
 // timeout_ns the kernel records a code in *err (host-mapped) and returns.

@@ -140,14 +140,45 @@ __global__ void __launch_bounds__(RR_WARPS * 32)
     for (int u = 0; u < U; ++u)
       o[u] = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
                         pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
-    const int nd = rr.dtd ? rr.Gt : 1;
+    const int nd = rr.fold ? rr.Gt : 1;
     for (int k = 0; k < nd; ++k) {
-      const int dr = dst0 + (rr.dtd ? k : rr.t);
+      const int dr = dst0 + (rr.fold ? k : rr.t);
       uint8_t* dst = static_cast<uint8_t*>(rr.table[(size_t)dr * rr.nwin + rr.dst_win]) + ooff;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
         if (v < nv) st_v4(dst + (size_t)v * 16, o[u]);
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// DTD all-gather within the TP group (MOE_F_NVLS): nseg segments of seg_bytes at
+// base_off + i * stride of window `win` of this rank go to the same offsets of every TP
+// rank's window — through the TP group's multicast mapping `mc` (one multimem.st,
+// replicated by NVSwitch: the sender's egress is the slice once whatever G_t), or, with
+// no multicast mapping (emulated ranks), one unicast store per TP peer. Bytes are copied
+// as 16-byte vectors, bit for bit.
+__global__ void __launch_bounds__(256)
+    tp_allgather_kernel(TpAllGather ag) {
+  const uint64_t nv = ag.seg_bytes / 16;
+  const uint64_t total = nv * (uint64_t)ag.nseg;
+  const uint8_t* src = static_cast<const uint8_t*>(ag.table[(size_t)ag.rank * ag.nwin + ag.win]);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t seg = i / nv, v = i - seg * nv;
+    const uint64_t off = ag.base_off + seg * ag.stride + v * 16;
+    const uint4 x = ld_nc_v4(src + off);
+    if (ag.mc) {
+      asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(static_cast<uint8_t*>(ag.mc) + off),
+                   "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w)
+                   : "memory");
+    } else {
+      for (int tp = 0; tp < ag.Gt; ++tp) {
+        const int r = ag.tp0 + tp;
+        if (r == ag.rank) continue;
+        st_v4(static_cast<uint8_t*>(ag.table[(size_t)r * ag.nwin + ag.win]) + off, x);
       }
     }
   }
@@ -168,6 +199,15 @@ __global__ void peer_wait_kernel(const uint32_t* flag, uint32_t epoch, int32_t* 
 }
 
 }  // namespace
+
+cudaError_t tp_allgather(const TpAllGather& ag, cudaStream_t s) {
+  const uint64_t total = ag.seg_bytes / 16 * (uint64_t)ag.nseg;
+  if (!total) return cudaSuccess;
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;  // grid-stride: a few waves of 256-thread CTAs
+  tp_allgather_kernel<<<(unsigned)blocks, 256, 0, s>>>(ag);
+  return cudaGetLastError();
+}
 
 cudaError_t peer_signal(uint32_t* flag, uint32_t epoch, cudaStream_t s) {
   peer_signal_kernel<<<1, 1, 0, s>>>(flag, epoch);

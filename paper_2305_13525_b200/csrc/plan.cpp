@@ -27,7 +27,7 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   if (world % tp_ep) { *why = "world % (g_tensor * g_expert) != 0"; return MOE_ERR_SHAPE; }
   if (c->tokens > (int64_t)1 << 30) { *why = "tokens must be < 2^30"; return MOE_ERR_SHAPE; }
   if (c->flags & ~(MOE_F_STATS | MOE_F_FORCED_ROUTING | MOE_F_TIMING | MOE_F_NCCL_EXCHANGE |
-                   MOE_F_CHECKPOINT | MOE_F_CAC | MOE_F_RANDOM_PRIORITY | MOE_F_AUX_LOSS)) {
+                   MOE_F_CHECKPOINT | MOE_F_CAC | MOE_F_RANDOM_PRIORITY | MOE_F_AUX_LOSS | MOE_F_NVLS)) {
     *why = "unknown flag bits";
     return MOE_ERR_ARG;
   }
@@ -67,6 +67,7 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->dtd = c->dtd != 0 && d->Gt > 1;
   d->forced = (c->flags & MOE_F_FORCED_ROUTING) != 0;
   d->peer = world > 1 && (c->flags & MOE_F_NCCL_EXCHANGE) == 0;
+  d->nvls = (c->flags & MOE_F_NVLS) != 0 && d->peer && d->dtd;
   d->ckpt = (c->flags & MOE_F_CHECKPOINT) != 0;
   d->cac = d->ckpt && (c->flags & MOE_F_CAC) != 0;
   d->rts = (c->flags & MOE_F_RANDOM_PRIORITY) != 0;
@@ -186,14 +187,16 @@ std::vector<moe_collective> make_schedule(const Dims& d) {
     const bool bwd = pass == 1;  // replay (pass 2) repeats the forward steps
     const int s_a2a1 = bwd ? 2 : 4, s_ag1 = bwd ? 3 : 5, s_red = bwd ? 7 : 8;
     const int s_a2a2 = bwd ? 8 : 9, s_ag2 = bwd ? 9 : 10;
+    // NVLS: a rank's all-gather egress is its own slice once (the switch replicates it)
+    const int64_t ag_x = d.nvls ? xe / g : xe * (g - 1) / g, ag_o = d.nvls ? O / g : O * (g - 1) / g;
     if (d.Gep > 1) push(MOE_COLL_A2A, pass, s_a2a1, d.Gep, a2a_buf, a2a_wire);
-    if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag1, d.Gt, xe, xe * (g - 1) / g);
+    if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag1, d.Gt, xe, ag_x);
     if (d.Gt > 1) {
       if (d.dtd) push(MOE_COLL_REDUCESCATTER, pass, s_red, d.Gt, xe, xe * (g - 1) / g);
       else push(MOE_COLL_ALLREDUCE, pass, s_red, d.Gt, xe, 2 * xe * (g - 1) / g);
     }
     if (d.Gep > 1) push(MOE_COLL_A2A, pass, s_a2a2, d.Gep, a2a_buf, a2a_wire);
-    if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag2, d.Gt, O, O * (g - 1) / g);
+    if (d.dtd) push(MOE_COLL_ALLGATHER, pass, s_ag2, d.Gt, O, ag_o);
   }
   return v;
 }

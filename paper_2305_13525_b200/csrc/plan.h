@@ -23,6 +23,7 @@ struct Dims {
   bool dtd;          // DTD in effect (requested and G_t > 1)
   bool forced;
   bool peer;         // world > 1 and the peer-memory exchange (not MOE_F_NCCL_EXCHANGE)
+  bool nvls;         // MOE_F_NVLS with DTD in effect: a2a of the own slice + multicast all-gather
   bool ckpt;         // MOE_F_CHECKPOINT
   bool cac;          // MOE_F_CAC (with ckpt)
   bool rts;          // MOE_F_RANDOM_PRIORITY

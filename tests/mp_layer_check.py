@@ -26,7 +26,8 @@ sys.path.insert(0, ROOT)
 
 from oracle import moe_oracle as O  # noqa: E402
 from paper_2305_13525_b200 import (MOE_F_AUX_LOSS, MOE_F_CAC, MOE_F_CHECKPOINT,  # noqa: E402
-                                   MOE_F_NCCL_EXCHANGE, MOE_F_RANDOM_PRIORITY, MoEConfig, MoELayer, synth)
+                                   MOE_F_NCCL_EXCHANGE, MOE_F_NVLS, MOE_F_RANDOM_PRIORITY, MoEConfig, MoEError,
+                                   MoELayer, synth)
 from tests.helpers import REL_L2_BAR, bf16_tensor, rel_l2, tensor_f64  # noqa: E402
 
 
@@ -64,11 +65,19 @@ def main():
     # (dtd, extra flags, key): DTD, vanilla, NCCL-exchange baseline, checkpointing with and without CAC
     modes = ((True, 0, True), (False, 0, False), (True, MOE_F_NCCL_EXCHANGE, "nccl"),
              (True, MOE_F_CHECKPOINT | MOE_F_CAC, "cac"), (True, MOE_F_CHECKPOINT, "ckpt"))
+    if a.gt > 1:  # DTD's all-gathers on NVLink SHARP multicast (NEXT #2)
+        modes += ((True, MOE_F_NVLS, "nvls"),)
     for dtd, extra, key in modes:
         cfg = MoEConfig.from_shape(shape, dtd=dtd)
         cfg = MoEConfig(cfg.tokens, cfg.hidden, cfg.ffn, cfg.experts, cfg.capacity_factor,
                         cfg.g_tensor, cfg.g_expert, cfg.dtd, cfg.flags | extra)
-        layer = MoELayer(cfg, world, rank, dev)
+        try:
+            layer = MoELayer(cfg, world, rank, dev)
+        except MoEError as e:
+            if key == "nvls" and "UNSUPPORTED" in str(e):
+                print(f"[rank {rank}] NVLS unavailable: {e}", flush=True)
+                continue
+            raise
         L = layer.layout
         s = L["d"] * a.gep + L["ep"]
         w1s, w2s = synth.shard_experts(w1_b, w2_b, shape, L["ep"], L["t"])
@@ -165,6 +174,18 @@ def main():
         failures.append(f"CAC replay issued {results['cac']['stats']['replay_calls']} collectives")
     if results["ckpt"]["stats"]["replay_calls"] != t_["stats"]["forward_calls"]:
         failures.append("plain checkpoint replay did not repeat the forward's collectives")
+    # ---- NVLS all-gathers: the same bits at the same positions as the folded DTD exchange,
+    # a2a bytes unchanged, all-gather egress 1 / (G_t - 1) of the folded one
+    if "nvls" in results:
+        nv = results["nvls"]
+        for k in ("y", "dx", "dwg", "dw1", "dw2"):
+            if not torch.equal(nv[k], t_[k]):
+                failures.append(f"NVLS != folded DTD (bitwise) for {k}")
+        if nv["stats"]["wire_bytes"]["a2a"] != t_["stats"]["wire_bytes"]["a2a"]:
+            failures.append("NVLS a2a bytes differ from DTD")
+        ag_f, ag_n = t_["stats"]["wire_bytes"]["allgather"], nv["stats"]["wire_bytes"]["allgather"]
+        if ag_n * (a.gt - 1) != ag_f:
+            failures.append(f"NVLS all-gather egress {ag_n} x {a.gt - 1} != folded {ag_f}")
     a2a_dtd = t_["stats"]["wire_bytes"]["a2a"]
     a2a_van = v["stats"]["wire_bytes"]["a2a"]
     if a2a_dtd * a.gt != a2a_van:

@@ -51,7 +51,7 @@ def test_status_strings():
     (dict(experts=65), "MOE_ERR_SHAPE"),                      # E <= 64
     (dict(tokens=0), "MOE_ERR_ARG"),
     (dict(capacity_factor=0.0), "MOE_ERR_ARG"),
-    (dict(flags=256), "MOE_ERR_ARG"),
+    (dict(flags=512), "MOE_ERR_ARG"),  # first unused flag bit
     (dict(flags=128, aux_loss_coef=-1.0), "MOE_ERR_ARG"),
     (dict(top_k=3), "MOE_ERR_ARG"),
     (dict(top_k=2, experts=1), "MOE_ERR_SHAPE"),
@@ -282,3 +282,23 @@ def test_peer_dtd_beyond_eight_tp_ranks_is_unsupported():
     assert ei.value.name == "MOE_ERR_UNSUPPORTED"
     moe_plan_layout(cfg.replace(flags=cfg.flags | MOE_F_NCCL_EXCHANGE), 16, 0)
     moe_plan_layout(cfg.replace(dtd=False), 16, 0)
+
+
+def test_nvls_plan_allgather_egress():
+    """MOE_F_NVLS (PAPER.md:1153-1158 with the all-gather on NVLink SHARP multicast): the same
+    collective calls and a2a bytes as folded DTD; each all-gather's wire bytes are the rank's
+    own slice once instead of G_t - 1 copies."""
+    from paper_2305_13525_b200 import MOE_F_NVLS
+    for gt, gep in ((2, 2), (4, 1), (4, 2)):
+        base = MoEConfig(tokens=4096, hidden=512, ffn=1024, experts=8, g_tensor=gt, g_expert=gep)
+        nv = MoEConfig(tokens=4096, hidden=512, ffn=1024, experts=8, g_tensor=gt, g_expert=gep,
+                       flags=base.flags | MOE_F_NVLS)
+        world = gt * gep
+        for rank in range(world):
+            a, b = moe_plan_collectives(base, world, rank), moe_plan_collectives(nv, world, rank)
+            assert [(c["kind"], c["pass"], c["step"]) for c in a] == [(c["kind"], c["pass"], c["step"]) for c in b]
+            for ca, cb in zip(a, b):
+                if ca["kind"] == "allgather":
+                    assert cb["wire_bytes"] * (gt - 1) == ca["wire_bytes"]
+                else:
+                    assert cb["wire_bytes"] == ca["wire_bytes"]

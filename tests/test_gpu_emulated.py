@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2305_13525_b200 import (MOE_F_AUX_LOSS, MOE_F_CAC, MOE_F_CHECKPOINT, MOE_F_RANDOM_PRIORITY,
+from paper_2305_13525_b200 import (MOE_F_NVLS, MOE_F_AUX_LOSS, MOE_F_CAC, MOE_F_CHECKPOINT, MOE_F_RANDOM_PRIORITY,
                                    EmuGroup, MoEComm, MoEError, MoELayer, moe_comm_plan_bytes,
                                    moe_plan_collectives, synth)
 from tests import emu
@@ -41,7 +41,17 @@ def test_emulated_exchange_parity(gt, gep):
     wl = emu.Workload(_shape(gt, gep))
     modes = {"dtd": wl.config(True), "van": wl.config(False),
              "cac": wl.config(True, MOE_F_CHECKPOINT | MOE_F_CAC), "ckpt": wl.config(True, MOE_F_CHECKPOINT)}
+    if gt > 1:  # the NVLS data flow (own-slice a2a, then a TP-group all-gather), unicast-emulated
+        modes["nvls"] = wl.config(True, MOE_F_NVLS)
     res = emu.run_modes(wl, modes, replay_keys=("cac", "ckpt"))
+    if gt > 1:
+        fails_nv = emu.bitwise_failures(res, "dtd", "nvls")
+        for r, rr in enumerate(res):
+            fails_nv += _ledger(rr["nvls"]["stats"], modes["nvls"], wl.world, r)
+            ag_f, ag_n = rr["dtd"]["stats"]["wire_bytes"]["allgather"], rr["nvls"]["stats"]["wire_bytes"]["allgather"]
+            if ag_n * (gt - 1) != ag_f:
+                fails_nv.append(f"rank {r}: NVLS all-gather egress {ag_n} x {gt - 1} != folded {ag_f}")
+        assert not fails_nv, "\n".join(fails_nv[:40])
     fails, errs = emu.oracle_failures(wl, res, "dtd")
     fails += emu.oracle_failures(wl, res, "van")[0]
     fails += (emu.bitwise_failures if gt <= 2 else emu.close_failures)(res, "dtd", "van")

@@ -15,9 +15,12 @@ run() {  # name, args...
 run 13b
 run 27b --config 2.7b
 run 67b_dtd --config 6.7b --gt 2
+run 67b_nvls --config 6.7b --gt 2 --nvls
 run 67b_van --config 6.7b --gt 2 --vanilla
 if [ $N -ge 4 ]; then
   run 27b_tp2 --config 2.7b --gt 2
   run 27b_tp4 --config 2.7b --gt 4
+  run 27b_tp4_nvls --config 2.7b --gt 4 --nvls
   run 27b_tp4_van --config 2.7b --gt 4 --vanilla
+  run 67b_tp2ep2_nvls --config 6.7b --gt 2 --nvls
 fi
