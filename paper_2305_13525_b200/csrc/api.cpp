@@ -364,7 +364,10 @@ PeerDst peer_dst(const moe_ctx* c, int win) {
   pd.nwin = c->comm->nwin;
   pd.win = win;
   pd.d = d.d; pd.ep = d.ep; pd.t = d.t; pd.Gt = d.Gt; pd.Gep = d.Gep; pd.El = d.El;
-  pd.dtd = d.dtd && !d.nvls ? 1 : 0;  // folded all-gather: write every TP rank of the destination
+  // folded all-gather: write every TP rank of the destination (DTD, and NVLS direct where the
+  // own group's rows take one multicast store); two-step NVLS sends the own slice to the same t
+  pd.dtd = d.dtd && (!d.nvls || d.nvls_direct) ? 1 : 0;
+  pd.mc = d.nvls_direct && !c->comm->mcwin.empty() ? c->comm->mcwin[win] : nullptr;
   return pd;
 }
 
@@ -479,6 +482,11 @@ moe_status barrier(moe_ctx* c, cudaStream_t st) {
   return MOE_OK;
 }
 
+// All-gather egress of a folded exchange: the G_t - 1 copies a rank writes itself, or under
+// NVLS direct (every destination is the own TP group) the one copy that goes through the
+// multicast mapping.
+int64_t ag_bytes(const Dims& d, int64_t folded) { return d.nvls_direct ? folded / (d.Gt - 1) : folded; }
+
 // MOE_F_NVLS: DTD's all-gather as its own step — this rank's slice of window `win`
 // (expert space [E_l][G_t][G_ep][C_s][H] or slot space [G_t][E][C_s][H]) goes once through
 // the TP group's multicast mapping (emulated ranks: a store per TP peer), then a barrier.
@@ -522,7 +530,8 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
   rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E; rr.H = d.H;
   rr.Cs = d.Cs;
   rr.dtd = d.dtd ? 1 : 0;
-  rr.fold = d.dtd && !d.nvls ? 1 : 0;
+  rr.fold = d.dtd && (!d.nvls || d.nvls_direct) ? 1 : 0;
+  rr.mc = d.nvls_direct && !c->comm->mcwin.empty() ? c->comm->mcwin[dst_win] : nullptr;
   CUDA_TRY(c, reduce_return(rr, st));
   c->stats.kernel_launches[MOE_K_COMM] += 1;
   TRY0(barrier(c, st));
@@ -530,8 +539,8 @@ moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_
   if (d.dtd) ledger(c, MOE_COLL_REDUCESCATTER, pass, xe * (d.Gt - 1) / d.Gt);
   else ledger(c, MOE_COLL_ALLREDUCE, pass, 2 * xe * (d.Gt - 1) / d.Gt);
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
-  if (d.nvls) TRY0(nvls_allgather(c, dst_win, false, pass, st));
-  else if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
+  if (d.nvls && !d.nvls_direct) TRY0(nvls_allgather(c, dst_win, false, pass, st));
+  else if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, ag_bytes(d, c->ret_bytes[2]));
   return MOE_OK;
 }
 
@@ -541,7 +550,7 @@ moe_status publish(moe_ctx* c, bool dispatch, int pass, cudaStream_t st) {
   TRY0(barrier(c, st));
   const int64_t* b = dispatch ? c->disp_bytes : c->ret_bytes;
   if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, b[1]);
-  if (d.dtd && !d.nvls) ledger(c, MOE_COLL_ALLGATHER, pass, b[2]);  // NVLS: nvls_allgather
+  if (d.dtd && (!d.nvls || d.nvls_direct)) ledger(c, MOE_COLL_ALLGATHER, pass, ag_bytes(d, b[2]));
   return MOE_OK;
 }
 
@@ -597,7 +606,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, pass, st));
-    if (d.nvls) TRY(nvls_allgather(c, c->comm->wx(rslot), true, pass, st));
+    if (d.nvls && !d.nvls_direct) TRY(nvls_allgather(c, c->comm->wx(rslot), true, pass, st));
   } else {
     Scope sc_(c, MOE_K_DISPATCH, st, 1);
     CUDA_TRY(c, dispatch(x, tok_of, count, ss, lo, hi, D, at<int32_t>(saved, sv.slot), d.T,
@@ -1075,7 +1084,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
     TRY(publish(c, true, 1, st));
-    if (d.nvls) TRY(nvls_allgather(c, moe_comm::W_DY, true, 1, st));
+    if (d.nvls && !d.nvls_direct) TRY(nvls_allgather(c, moe_comm::W_DY, true, 1, st));
   } else if (fused_dx) {
     // B1 + the head of B10 in one launch (dl, extension operands, dropped rows)
     Scope sc_(c, MOE_K_COMBINE_BWD, st, 1);
@@ -1131,7 +1140,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       rr.dst_win = moe_comm::W_DS;
       rr.d = d.d; rr.ep = d.ep; rr.t = d.t; rr.Gt = d.Gt; rr.Gep = d.Gep; rr.El = d.El; rr.E = d.E;
       rr.H = d.H; rr.Cs = d.Cs; rr.dtd = d.dtd ? 1 : 0;
-      rr.fold = d.dtd && !d.nvls ? 1 : 0;
+      rr.fold = d.dtd && (!d.nvls || d.nvls_direct) ? 1 : 0;
+      rr.mc = d.nvls_direct && !c->comm->mcwin.empty() ? c->comm->mcwin[moe_comm::W_DS] : nullptr;
       CUDA_TRY(c, reduce_return(rr, st));
       c->stats.kernel_launches[MOE_K_COMM] += 1;
     }
@@ -1143,8 +1153,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     if (d.dtd) ledger(c, MOE_COLL_REDUCESCATTER, 1, xe * (d.Gt - 1) / d.Gt);
     else ledger(c, MOE_COLL_ALLREDUCE, 1, 2 * xe * (d.Gt - 1) / d.Gt);
     if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
-    if (d.nvls) TRY(nvls_allgather(c, moe_comm::W_DS, false, 1, st));
-    else if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
+    if (d.nvls && !d.nvls_direct) TRY(nvls_allgather(c, moe_comm::W_DS, false, 1, st));
+    else if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, ag_bytes(d, c->ret_bytes[2]));
   } else if (d.peer) {
     // B7-B9 (TP reduction + return pieces) on the side stream, overlapping the
     // weight-gradient GEMMs, which do not feed them

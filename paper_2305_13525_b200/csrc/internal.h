@@ -158,6 +158,8 @@ struct ReduceReturn {
   int64_t Cs;
   int dtd;   // reduce only the rank's own slot slice
   int fold;  // and store it to every TP rank of the source (folded all-gather), else to the same t
+  void* mc;  // MOE_F_NVLS direct: multicast mapping of dst_win over the own TP group (fold: rows
+             // for the own EP group are stored once through it), or null
 };
 cudaError_t reduce_return(const ReduceReturn& rr, cudaStream_t s);
 // (peer.cu) DTD all-gather in the TP group over NVLink SHARP multicast (MOE_F_NVLS):
@@ -189,6 +191,8 @@ struct PeerDst {
   int nwin, win;
   int d, ep, t, Gt, Gep, El;
   int dtd;
+  void* mc;  // MOE_F_NVLS direct: multicast mapping of `win` over this rank's TP group, or null;
+             // with dtd, rows for the own EP group go once through it instead of G_t stores
 };
 // F3 + F4 (+F5): gather x rows of slices [t_lo, t_hi) straight into the peers' windows.
 cudaError_t dispatch_peer(const void* x, const int32_t* tok_of, const int32_t* count,

@@ -140,14 +140,19 @@ __global__ void __launch_bounds__(RR_WARPS * 32)
     for (int u = 0; u < U; ++u)
       o[u] = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
                         pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
-    const int nd = rr.fold ? rr.Gt : 1;
+    const bool mc = rr.fold && rr.mc && src == rr.ep;  // own group: one multicast store
+    const int nd = mc ? 1 : (rr.fold ? rr.Gt : 1);
     for (int k = 0; k < nd; ++k) {
       const int dr = dst0 + (rr.fold ? k : rr.t);
-      uint8_t* dst = static_cast<uint8_t*>(rr.table[(size_t)dr * rr.nwin + rr.dst_win]) + ooff;
+      uint8_t* dst = mc ? static_cast<uint8_t*>(rr.mc) + ooff
+                        : static_cast<uint8_t*>(rr.table[(size_t)dr * rr.nwin + rr.dst_win]) + ooff;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
-        if (v < nv) st_v4(dst + (size_t)v * 16, o[u]);
+        if (v < nv) {
+          if (mc) st_mc_v4(dst + (size_t)v * 16, o[u]);
+          else st_v4(dst + (size_t)v * 16, o[u]);
+        }
       }
     }
   }
@@ -171,9 +176,7 @@ __global__ void __launch_bounds__(256)
     const uint64_t off = ag.base_off + seg * ag.stride + v * 16;
     const uint4 x = ld_nc_v4(src + off);
     if (ag.mc) {
-      asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(static_cast<uint8_t*>(ag.mc) + off),
-                   "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w)
-                   : "memory");
+      st_mc_v4(static_cast<uint8_t*>(ag.mc) + off, x);
     } else {
       for (int tp = 0; tp < ag.Gt; ++tp) {
         const int r = ag.tp0 + tp;

@@ -211,8 +211,32 @@ __device__ __forceinline__ uint8_t* peer_row(const PeerDst& pd, int tt, int e, i
   return base + ((((size_t)el * pd.Gt + tt) * pd.Gep + pd.ep) * ss.Cs + cs) * ss.H * 2;
 }
 
+// Row offset of slot (tt, e, cs) in the expert-space window (the same on every TP rank).
+__device__ __forceinline__ size_t peer_off(const PeerDst& pd, int tt, int e, int64_t cs, const SlotSpace& ss) {
+  const int el = e % pd.El;
+  return ((((size_t)el * pd.Gt + tt) * pd.Gep + pd.ep) * ss.Cs + cs) * ss.H * 2;
+}
+
+// Destinations of one row: G_t TP ranks (DTD fold), one multicast store when the owner
+// group is this rank's own and a multicast mapping exists (MOE_F_NVLS direct), or the
+// same-t rank (vanilla / two-step NVLS). Returns the count; *mc says "multicast".
+__device__ __forceinline__ int row_dsts(const PeerDst& pd, int tt, int e, int64_t cs, const SlotSpace& ss,
+                                        bf16* (&dsts)[8], bool* mc) {
+  *mc = pd.dtd && pd.mc && e / pd.El == pd.ep;
+  if (*mc) {
+    dsts[0] = reinterpret_cast<bf16*>(static_cast<uint8_t*>(pd.mc) + peer_off(pd, tt, e, cs, ss));
+    return 1;
+  }
+  const int nd = pd.dtd ? pd.Gt : 1;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    dsts[k] = k < nd ? reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)) : nullptr;
+  return nd;
+}
+
 // One warp per slot row: the x row (or zeros) is read once and stored to every
-// destination rank (1 for vanilla, G_t for DTD) with 16-byte stores over NVLink.
+// destination rank (1 for vanilla, G_t for DTD, one multicast store for the own group
+// under MOE_F_NVLS) with 16-byte stores over NVLink.
 __global__ void __launch_bounds__(WARPS * 32)
     dispatch_peer_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ tok_of,
                          const int32_t* __restrict__ count, SlotSpace ss, int t_lo, int64_t rows,
@@ -229,12 +253,10 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int nv = ss.H / 8;
   const bool full = c < count[e];
   const bf16* src = full ? x + (size_t)(tok_of[(size_t)e * ss.C + c] / ss.K) * ss.H : nullptr;
-  const int nd = pd.dtd ? pd.Gt : 1;
   constexpr int MAXD = 8;  // destination rows resolved once per row (G_t <= 8)
   bf16* dsts[MAXD];
-#pragma unroll
-  for (int k = 0; k < MAXD; ++k)
-    dsts[k] = k < nd ? reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)) : nullptr;
+  bool mc;
+  const int nd = row_dsts(pd, tt, e, cs, ss, dsts, &mc);
   constexpr int U = 8;
   for (int v0 = 0; v0 < nv; v0 += 32 * U) {
     uint4 buf[U];
@@ -249,7 +271,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
-        if (v < nv) st_v4(dsts[k] + (size_t)v * 8, buf[u]);
+        if (v < nv) {
+          if (mc) st_mc_v4(dsts[k] + (size_t)v * 8, buf[u]);
+          else st_v4(dsts[k] + (size_t)v * 8, buf[u]);
+        }
       }
     }
   }
@@ -282,12 +307,10 @@ __global__ void __launch_bounds__(WARPS * 32)
   const bf16* dyr = dy + (size_t)t * ss.H;
   const bf16* orow = O + row;
   const int nv = ss.H / 8;
-  const int nd = mine ? (pd.dtd ? pd.Gt : 1) : 0;
   constexpr int MAXD = 8;
   bf16* dsts[MAXD];
-#pragma unroll
-  for (int k = 0; k < MAXD; ++k)
-    dsts[k] = k < nd ? reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)) : nullptr;
+  bool mc = false;
+  const int nd = mine ? row_dsts(pd, tt, e, cs, ss, dsts, &mc) : 0;
   float acc = 0.f;
   constexpr int U = 4;
   for (int v0 = 0; v0 < nv; v0 += 32 * U) {
@@ -319,7 +342,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = v0 + u * 32 + lane;
-        if (v < nv) st_v4(dsts[k] + (size_t)v * 8, w[u]);
+        if (v < nv) {
+          if (mc) st_mc_v4(dsts[k] + (size_t)v * 8, w[u]);
+          else st_v4(dsts[k] + (size_t)v * 8, w[u]);
+        }
       }
     }
   }
@@ -342,10 +368,14 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int e = (int)(rem / ss.Cs);
   const int64_t cs = rem % ss.Cs;
   if ((int64_t)tt * ss.Cs + cs < count[e]) return;
-  const int nd = pd.dtd ? pd.Gt : 1;
+  bf16* dsts[8];
+  bool mc;
+  const int nd = row_dsts(pd, tt, e, cs, ss, dsts, &mc);
   for (int k = 0; k < nd; ++k)
-    copy_row<true>(nullptr, reinterpret_cast<bf16*>(peer_row(pd, tt, e, cs, ss, pd.dtd ? k : pd.t)),
-                   ss.H / 8, lane);
+    for (int v = lane; v < ss.H / 8; v += 32) {
+      if (mc) st_mc_v4(dsts[k] + (size_t)v * 8, make_uint4(0, 0, 0, 0));
+      else st_v4(dsts[k] + (size_t)v * 8, make_uint4(0, 0, 0, 0));
+    }
   __threadfence_system();
 }
 

@@ -68,6 +68,7 @@ moe_status make_dims(const moe_config* c, int world, int rank, Dims* d, std::str
   d->forced = (c->flags & MOE_F_FORCED_ROUTING) != 0;
   d->peer = world > 1 && (c->flags & MOE_F_NCCL_EXCHANGE) == 0;
   d->nvls = (c->flags & MOE_F_NVLS) != 0 && d->peer && d->dtd;
+  d->nvls_direct = d->nvls && d->Gep == 1;
   d->ckpt = (c->flags & MOE_F_CHECKPOINT) != 0;
   d->cac = d->ckpt && (c->flags & MOE_F_CAC) != 0;
   d->rts = (c->flags & MOE_F_RANDOM_PRIORITY) != 0;

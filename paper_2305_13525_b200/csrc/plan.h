@@ -23,7 +23,10 @@ struct Dims {
   bool dtd;          // DTD in effect (requested and G_t > 1)
   bool forced;
   bool peer;         // world > 1 and the peer-memory exchange (not MOE_F_NCCL_EXCHANGE)
-  bool nvls;         // MOE_F_NVLS with DTD in effect: a2a of the own slice + multicast all-gather
+  bool nvls;         // MOE_F_NVLS with DTD in effect
+  bool nvls_direct;  //   G_ep == 1: every destination is the own TP group -> the fused exchange
+                     //   kernels store once through the multicast mapping (no extra step);
+                     //   else: a2a of the own slice, then a multicast all-gather step
   bool ckpt;         // MOE_F_CHECKPOINT
   bool cac;          // MOE_F_CAC (with ckpt)
   bool rts;          // MOE_F_RANDOM_PRIORITY

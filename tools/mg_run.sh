@@ -6,6 +6,7 @@ P=gpurun_out/mg$N
 mkdir -p $P
 nvidia-smi topo -m > $P/topo.txt 2>&1
 timeout -s KILL 1200 python -m pytest tests/test_gpu_multi.py -q -rs > $P/pytest.log 2>&1; echo pytest=$?
+timeout -s KILL 600 python -m pytest tests/test_gpu_emulated.py -q -x -m gpu -k "exchange_parity" > $P/emu.log 2>&1; echo emu=$?
 run() {  # name, args...
   local name=$1; shift
   timeout -s KILL 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
