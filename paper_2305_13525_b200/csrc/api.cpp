@@ -9,6 +9,7 @@
 // ncclAllGather per local expert over the TP communicator, and AR + drop on the
 // return path is an in-place ncclReduceScatter (R11, R12). Vanilla and
 // DTD feed the expert GEMMs the same rows in the same positions.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
@@ -44,6 +45,7 @@ struct moe_ctx {
   uint64_t priority_seed = 0;  // MOE_F_RANDOM_PRIORITY key (moe_set_priority_seed)
   bool no_fused_dx = false;    // MOE_NO_FUSED_DX=1: B10 as a separate kernel (A/B, tests)
   bool no_fused_combine = false;  // MOE_NO_FUSED_COMBINE=1: F11 as a separate kernel
+  bool no_gemm_signal = false;    // MOE_NO_GEMM_SIGNAL=1: GEMM2 parts as separate launches (A/B)
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): this layer's piece lists over the comm's windows
@@ -55,6 +57,10 @@ struct moe_ctx {
   bool overlap = true;             // MOE_NO_OVERLAP=1: serial return exchanges (A/B knob)
   cudaEvent_t ev[4] = {};
   cudaEvent_t evp[4] = {};  // GEMM2 parts (G_t = 1 return overlap)
+  // GEMM2 part-completion flags (device, comm arena): cnt[4] then flag[4]; the side stream
+  // waits on flag values (cuStreamWaitValue32) instead of part boundaries between launches
+  int32_t* gsig = nullptr;
+  uint32_t gsig_epoch = 0;
   int64_t disp_bytes[3] = {0, 0, 0}, ret_bytes[3] = {0, 0, 0};  // by Piece::kind
   std::unordered_map<const void*, std::pair<int, uint64_t>> saved_slot;  // saved -> (ring slot, gen)
   const void* replayed = nullptr;  // MOE_F_CHECKPOINT: saved blob whose G/A sit in scratch
@@ -254,6 +260,20 @@ moe_status ag_slot(moe_ctx* c, int pass, void* O, cudaStream_t st) {
   return MOE_OK;
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda); null if absent
+using StreamWait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamWait32 stream_wait32() {
+  static const StreamWait32 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return StreamWait32(nullptr);
+    return reinterpret_cast<StreamWait32>(f);
+  }();
+  return fn;
+}
+
 moe_status gemm(moe_ctx* c, const GemmArgs& g, cudaStream_t st) {
   const char* why = "";
   if (c) {
@@ -341,6 +361,9 @@ moe_status setup_peer(moe_ctx* c) {
   if (!c->d_ret_local) return fail(MOE_ERR_STATE, "communicator piece arena exhausted (too many layers)");
   if (!loc.empty())
     CUDA_TRY(c, cudaMemcpy(c->d_ret_local, loc.data(), sizeof(Piece) * loc.size(), cudaMemcpyHostToDevice));
+  c->gsig = reinterpret_cast<int32_t*>(comm_pieces(m, (8 * sizeof(int32_t) + sizeof(Piece) - 1) / sizeof(Piece)));
+  if (!c->gsig) return fail(MOE_ERR_STATE, "communicator piece arena exhausted (too many layers)");
+  CUDA_TRY(c, cudaMemset(c->gsig, 0, 8 * sizeof(int32_t)));
   CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->evp[i], cudaEventDisableTiming));
@@ -668,6 +691,33 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     // pieces are exposed
     const int P = c->overlap ? (d.El < 4 ? d.El : 4) : 1;
     const size_t rows = (size_t)d.R * d.H;
+    if (P > 1 && stream_wait32() && !c->no_gemm_signal) {
+      // one GEMM2 launch (no per-part tail waves); each part's last tile raises its flag
+      // and the side stream's copy engines start that part's return pieces (F9)
+      GemmSignal gs;
+      gs.cnt = c->gsig;
+      gs.flag = reinterpret_cast<uint32_t*>(c->gsig + 4);
+      gs.epoch = ++c->gsig_epoch;
+      gs.nparts = P;
+      for (int q = 0; q <= P; ++q) gs.part_b[q] = q * d.El / P;
+      GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+      g2.sig = &gs;
+      TRY(gemm(c, g2, st));
+      // the waits go in after the GEMM launch: a stream-ordered value wait may block a
+      // hardware queue shared with other streams, so the work it waits for must already
+      // be enqueued (same rule as an event wait)
+      for (int q = 0; q < P; ++q) {
+        if (gs.part_b[q + 1] <= gs.part_b[q]) continue;
+        const CUresult r = stream_wait32()(c->side, reinterpret_cast<CUdeviceptr>(gs.flag + q), gs.epoch,
+                                           CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) {
+          c->poisoned = true;
+          return fail(MOE_ERR_CUDA, "cuStreamWaitValue32 failed");
+        }
+        Scope sx_(c, MOE_K_XFER, c->side, 0);
+        TRY(exchange_ce(c, Y, c->comm->wo(rslot), gs.part_b[q], gs.part_b[q + 1], c->side));
+      }
+    } else
     for (int part = 0; part < P; ++part) {
       const int e0 = part * d.El / P, e1 = (part + 1) * d.El / P;
       if (e1 <= e0) continue;
@@ -812,6 +862,8 @@ moe_status make_ctx(const moe_config* cfg, moe_comm* m, int world, int rank, voi
     c->no_fused_combine = nc && nc[0] == '1';
     const char* no = std::getenv("MOE_NO_OVERLAP");
     c->overlap = !(no && no[0] == '1');
+    const char* ns = std::getenv("MOE_NO_GEMM_SIGNAL");
+    c->no_gemm_signal = ns && ns[0] == '1';
   }
   c->d = d;
   c->cfg = *cfg;

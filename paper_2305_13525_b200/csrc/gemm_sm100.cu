@@ -49,6 +49,7 @@ struct Params {
   bf16* D;
   bf16* aux;
   GateDxArgs g;  // EPI_SCATTER / EPI_COMBINE
+  GemmSignal sig;  // sig.cnt != null: per-part completion flags (EPI_STORE)
 };
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
@@ -354,6 +355,21 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(smem_u32(&bars[2 * STAGES2 + 2 + acc]), 0);
+      if (EPI == EPI_STORE && p.sig.cnt) {
+        // every epilogue warp of this CTA has stored its rows of the tile
+        asm volatile("bar.sync 1, %0;" ::"r"(EW * 32) : "memory");
+        if (ew == 0 && lane == 0) {
+          int q = 0;
+          while (q + 1 < p.sig.nparts && b >= p.sig.part_b[q + 1]) ++q;
+          const int target = (p.sig.part_b[q + 1] - p.sig.part_b[q]) * tiles_mn * 2;
+          __threadfence_system();
+          if (atomicAdd(&p.sig.cnt[q], 1) == target - 1) {
+            p.sig.cnt[q] = 0;
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.sig.flag + q), "r"(p.sig.epoch) : "memory");
+          }
+        }
+      }
       if (ew == 0 && lane == 0) { PROF_ADD(4, w4); PROF_CNT(6); }
     }
   }
@@ -466,6 +482,14 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   p.D = static_cast<bf16*>(a.D);
   p.aux = static_cast<bf16*>(a.aux);
   p.g = a.gdx ? *a.gdx : GateDxArgs{};
+  p.sig = GemmSignal{};
+  if (a.sig) {
+    if (a.epilogue != EPI_STORE || a.sig->nparts < 1 || a.sig->nparts > 4 || a.sig->part_b[a.sig->nparts] != a.batch) {
+      *why = "completion signal: plain epilogue, 1-4 parts covering the batch";
+      return cudaErrorNotSupported;
+    }
+    p.sig = *a.sig;
+  }
   if (a.epilogue == EPI_COMBINE && !a.gdx) {
     *why = "combine epilogue needs its gate arguments";
     return cudaErrorNotSupported;

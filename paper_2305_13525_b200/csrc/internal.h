@@ -30,6 +30,19 @@ struct GateDxArgs {
 // y[tok_of[e][c]] = bf16(p_t * acc) for kept slots (F11 fused; uses tok_of, count, C,
 // prob and dx = y of GateDxArgs).
 
+// Tile-completion signal (G_t = 1 return overlap): the batches [part_b[q], part_b[q+1]) form
+// part q; when the last CTA finishes its share of part q's tiles (stores visible at system
+// scope), flag[q] = epoch (release) — a stream waiting on that value (cuStreamWaitValue32)
+// starts the part's copy-engine transfers while the same GEMM launch computes the next
+// parts. cnt[q] counts CTA tile completions and is reset by the last arrival.
+struct GemmSignal {
+  int32_t* cnt = nullptr;  // [4], zero between launches
+  uint32_t* flag = nullptr;  // [4]
+  uint32_t epoch = 0;
+  int nparts = 0;
+  int part_b[5] = {0, 0, 0, 0, 0};
+};
+
 struct GemmArgs {
   int batch, M, N, K;
   const void* A;
@@ -44,6 +57,7 @@ struct GemmArgs {
   // e.g. the rows of one source rank inside [E_l][G_ep][C]).
   int64_t a_bs = 0, d_bs = 0;
   const GateDxArgs* gdx = nullptr;  // EPI_SCATTER / EPI_COMBINE only
+  const GemmSignal* sig = nullptr;  // EPI_STORE only: per-part completion flags
 };
 
 // tcgen05 / TMEM / TMA kernel (the product path).
