@@ -485,6 +485,36 @@ moe_status gemm_rows(moe_ctx* c, GemmArgs g, int s0, int s1, int64_t a_ld, int64
   return gemm(c, g, st);
 }
 
+// G_t = 1 split exchange, GEMM1 / B4: the own source block, then the remote blocks in
+// arrival order (me-1, me-2, ...) in groups of g, each group one launch after its pieces
+// are in. g = 1 unless one block is too few tiles for the persistent grid (EP8: 2 local
+// experts x 4 x 32 = 256 tiles = 3.5 waves of 74 CTA pairs, ~13 % tail): then g blocks
+// per launch bring it to >= ~6 waves; blocks still arrive faster than they are consumed.
+moe_status gemm_sources(moe_ctx* c, const GemmArgs& g, uint32_t sig, int64_t a_ld, int64_t d_ld, cudaStream_t st) {
+  const Dims& d = c->d;
+  TRY0(gemm_rows(c, g, d.ep, d.ep + 1, a_ld, d_ld, st));  // own block overlaps the copy engines
+  const int64_t tiles = (int64_t)d.El * ((d.C + 255) / 256) * ((g.N + 255) / 256);
+  const int64_t want = 6 * 74;
+  int grp = tiles > 0 ? (int)((want + tiles - 1) / tiles) : 1;
+  if (grp < 1) grp = 1;
+  for (int k0 = 1; k0 < d.Gep; k0 += grp) {
+    const int k1 = k0 + grp < d.Gep ? k0 + grp : d.Gep;
+    {
+      Scope sc_(c, MOE_K_COMM, st, 0);
+      for (int k = k0; k < k1; ++k) TRY0(wait_source(c, (d.ep - k + d.Gep) % d.Gep, sig, st));
+    }
+    // sources me-k1+1 .. me-k0 (mod G_ep): contiguous unless they wrap past 0
+    const int lo = d.ep - (k1 - 1), hi = d.ep - k0 + 1;  // [lo, hi) before the wrap
+    if (lo >= 0) {
+      TRY0(gemm_rows(c, g, lo, hi, a_ld, d_ld, st));
+    } else {
+      if (hi > 0) TRY0(gemm_rows(c, g, 0, hi, a_ld, d_ld, st));
+      TRY0(gemm_rows(c, g, lo + d.Gep, hi > 0 ? d.Gep : hi + d.Gep, a_ld, d_ld, st));
+    }
+  }
+  return MOE_OK;
+}
+
 // G_t > 1: barrier (every TP partial complete), fused TP reduction + return exchange,
 // barrier (every destination written). Same ledger as the NCCL-mode RS/AR + a2a (+AG).
 moe_status tp_return(moe_ctx* c, int pass, int src_win, int dst_win, cudaStream_t st);
@@ -657,15 +687,7 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
   if (split) {
     // own block first (already in place), then each source block as its pieces land
     // (source me-k sends to me as its k-th destination)
-    TRY(gemm_rows(c, g1, d.ep, d.ep + 1, d.H, d.Fl, st));
-    for (int k = 1; k < d.Gep; ++k) {
-      const int src = (d.ep - k + d.Gep) % d.Gep;
-      {
-        Scope sc_(c, MOE_K_COMM, st, 0);
-        TRY(wait_source(c, src, sig, st));
-      }
-      TRY(gemm_rows(c, g1, src, src + 1, d.H, d.Fl, st));
-    }
+    TRY(gemm_sources(c, g1, sig, d.H, d.Fl, st));
     if (d.ckpt) {  // CAC stash of the first collective's output
       Scope sc_(c, MOE_K_COMM, st, 0);
       CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.X), X, (size_t)d.El * d.R * d.H * 2,
@@ -1158,15 +1180,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   // B4 dHpre = (dY W2) * G; B5 dXpart = dHpre W1; B6 dW2 = dY^T A, dW1 = dHpre^T X
   GemmArgs g4{d.El, (int)d.R, d.Fl, d.H, dY, 0, w2, 1, dH, EPI_DGELU, const_cast<void*>(G)};
   if (split) {
-    TRY(gemm_rows(c, g4, d.ep, d.ep + 1, d.H, d.Fl, st));  // own block overlaps the copy engines
-    for (int k = 1; k < d.Gep; ++k) {
-      const int src = (d.ep - k + d.Gep) % d.Gep;
-      {
-        Scope sc_(c, MOE_K_COMM, st, 0);
-        TRY(wait_source(c, src, sig, st));
-      }
-      TRY(gemm_rows(c, g4, src, src + 1, d.H, d.Fl, st));
-    }
+    TRY(gemm_sources(c, g4, sig, d.H, d.Fl, st));
   } else {
     TRY(gemm(c, g4, st));
   }
