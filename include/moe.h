@@ -315,6 +315,10 @@ moe_status moe_set_priority_seed(moe_ctx* ctx, uint64_t seed);
  * synchronizes the ctx's last stream. */
 moe_status moe_stats_get(moe_ctx* ctx, moe_stats* out);
 moe_status moe_stats_reset(moe_ctx* ctx);
+/* MOE_F_TIMING's per-class CUDA events on (on != 0) or off for the following calls of
+ * this ctx (the events sit between kernel launches, so a throughput measurement turns
+ * them off and a per-class breakdown turns them on). Without MOE_F_TIMING: MOE_ERR_STATE. */
+moe_status moe_set_timing(moe_ctx* ctx, int on);
 
 moe_status moe_destroy(moe_ctx* ctx);
 

@@ -75,7 +75,7 @@ class _AdamW(ctypes.Structure):
 
 EXPORTS = ("moe_plan_layout", "moe_plan_bytes", "moe_plan_collectives", "moe_get_unique_id",
            "moe_create", "moe_forward", "moe_backward", "moe_forward_replay", "moe_routing", "moe_stats_get",
-           "moe_stats_reset", "moe_destroy", "moe_status_string", "moe_last_error_detail",
+           "moe_stats_reset", "moe_set_timing", "moe_destroy", "moe_status_string", "moe_last_error_detail",
            "moe_gemm_bf16", "moe_adamw_plan", "moe_adamw_step", "moe_aux_loss", "moe_set_priority_seed",
            "moe_comm_plan_bytes", "moe_comm_create", "moe_comm_destroy", "moe_create_on_comm",
            "moe_emu_group_create", "moe_emu_group_destroy", "moe_comm_create_emulated")
@@ -107,6 +107,7 @@ def lib() -> ctypes.CDLL:
     L.moe_routing.argtypes = [P, P, P, P, P, P, P, P]
     L.moe_stats_get.argtypes = [P, ctypes.POINTER(_Stats)]
     L.moe_stats_reset.argtypes = [P]
+    L.moe_set_timing.argtypes = [P, I]
     L.moe_destroy.argtypes = [P]
     L.moe_status_string.argtypes = [I]
     L.moe_status_string.restype = ctypes.c_char_p
@@ -387,6 +388,9 @@ class MoELayer:
 
     def moe_stats_reset(self):
         _check(lib().moe_stats_reset(self.ctx))
+
+    def moe_set_timing(self, on: bool):
+        _check(lib().moe_set_timing(self.ctx, 1 if on else 0))
 
     def close(self):
         if getattr(self, "ctx", None) is not None and self.ctx.value:

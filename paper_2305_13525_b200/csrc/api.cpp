@@ -1394,6 +1394,13 @@ moe_status moe_stats_reset(moe_ctx* c) {
   return MOE_OK;
 }
 
+moe_status moe_set_timing(moe_ctx* c, int on) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  if (!(c->cfg.flags & MOE_F_TIMING)) return fail(MOE_ERR_STATE, "moe_set_timing needs MOE_F_TIMING");
+  c->timing = on != 0;
+  return MOE_OK;
+}
+
 moe_status moe_gemm_bf16(int batch, int M, int N, int K, const void* A, int a_mn, const void* B,
                          int b_mn, void* D, int epilogue, void* aux, int impl, void* stream) {
   if (batch < 0 || M < 0 || N < 0 || K < 0) return fail(MOE_ERR_ARG, "negative size");

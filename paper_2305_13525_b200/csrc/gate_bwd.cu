@@ -593,6 +593,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a programmatic dependent
 
   if (warp == 4) {
     if (lane == 0) {
@@ -812,9 +813,17 @@ cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, i
   if (nsplit > (kb + 3) / 4) nsplit = (kb + 3) / 4;  // >= 4 k-blocks per CTA
   if (nsplit > max_split) nsplit = max_split;
   if (nsplit < 1) nsplit = 1;
-  dwtc::dwg_tc_kernel<<<(unsigned)(mtiles * nsplit), dwtc::THREADS, dwtc::SMEM, s>>>(
-      ta, tb, rows, H, E, mtiles, nsplit, partial, counters, dwg);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(mtiles * nsplit));
+  cfg.blockDim = dim3(dwtc::THREADS);
+  cfg.dynamicSmemBytes = dwtc::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];  // the prologue overlaps the tail of the weight-gradient GEMM
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dwtc::dwg_tc_kernel, ta, tb, rows, H, E, mtiles, nsplit, partial, counters, dwg);
 }
 
 cudaError_t gate_dwg(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,

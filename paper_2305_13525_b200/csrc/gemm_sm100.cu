@@ -159,6 +159,12 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int tiles_mn = p.tiles_m * p.tiles_n;
+  // Programmatic dependent launch: the prologue above (barriers, TMEM, descriptor
+  // prefetch) may overlap the tail of the previous kernel in the stream; every global
+  // access below waits for its completion, and the next kernel may be scheduled as
+  // this grid's CTAs exit.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -387,6 +393,10 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
 
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+const bool g_pdl = [] {  // MOE_NO_PDL=1: plain stream serialization (A/B)
+  const char* e = std::getenv("MOE_NO_PDL");
+  return !(e && e[0] == '1');
+}();
 int g_num_sms = 0;
 std::once_flag g_once;
 cudaError_t g_init_err = cudaSuccess;
@@ -435,13 +445,15 @@ cudaError_t launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensor
   cfg.blockDim = dim3(threads2(EPI));
   cfg.dynamicSmemBytes = SMEM2_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = 2;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k, ta, tb, ta2, tb2, p);
 }
 
