@@ -69,7 +69,7 @@ def main():
     if os.path.exists(os.path.join(SRC, "launches.csv")):
         subprocess.run(["cp", os.path.join(SRC, "launches.csv"), os.path.join(OUT, f"{PFX}_launches.csv")], check=True)
         open(os.path.join(OUT, f"{PFX}_launch_table.md"), "w").write(launch_table(os.path.join(SRC, "launches.csv")) + "\n")
-    for rep, name in (("gemm_full", "gemm"), ("other_full", "other"), ("optim_full", "optim")):
+    for rep, name in (("gemm_full", "gemm"), ("other_full", "other"), ("small_full", "small"), ("optim_full", "optim")):
         p = os.path.join(SRC, rep + ".ncu-rep")
         if os.path.exists(p):
             ncu_summary(p, os.path.join(OUT, f"{PFX}_{name}_ncu_summary.txt"))
