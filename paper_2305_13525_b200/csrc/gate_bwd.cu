@@ -661,7 +661,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (h < H) {
       float* prow = partial + ((size_t)split * H + h) * E;
-      for (int j = 0; j < E; ++j) prow[j] = v[j];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < E) prow[j] = v[j];
     }
     __threadfence();
     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -670,11 +672,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (last) {  // every split of this h tile is in: sum in split order
       __threadfence();
       if (h < H) {
-        for (int j = 0; j < E; ++j) {
-          float sum = 0.f;
-          for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(partial + ((size_t)sp * H + h) * E + j);
-          dwg[(size_t)h * E + j] = sum;
+        // sum over splits in split order per j; the loads of several splits are issued
+        // together (a load -> add chain per (j, split) made this tail ~half the kernel)
+        float acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll 4
+        for (int sp = 0; sp < nsplit; ++sp) {
+          const float* pr = partial + ((size_t)sp * H + h) * E;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < E) acc[j] += __ldcg(pr + j);
         }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < E) dwg[(size_t)h * E + j] = acc[j];
       }
       if (threadIdx.x == 0) cnt[mt] = 0;
     }
