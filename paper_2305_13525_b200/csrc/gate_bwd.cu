@@ -16,10 +16,6 @@
 namespace moe {
 namespace {
 
-__device__ __forceinline__ size_t slot_row2(const SlotSpace& ss, int e, int64_t c) {
-  const int64_t tt = c / ss.Cs, cs = c - tt * ss.Cs;
-  return ((size_t)(tt * ss.E + e) * ss.Cs + cs) * ss.H;
-}
 
 // ------------------------------------------------------------------ Wg -> B' fragments
 // B'[k][h] for k in [0, 3*EPK): block 0 = hi(Wg), 1 = hi(Wg), 2 = lo(Wg) (paired with
@@ -49,6 +45,84 @@ __global__ void wg_pack_kernel(const float* __restrict__ wg, int H, int E, int E
   packed[i * 2 + 1] = pack2(val(k0 + 8), val(k0 + 9));
 }
 
+// ------------------------------------------------------------------ dl, grow
+// Warp per token, every token in flight at once: dl_tj from the saved logits (softmax
+// backward; top-2 through the renormalised weights w_k = s_ek / (s_e1 + s_e2), R22; + the
+// aux-loss term, R21) with lane j holding experts j, j + 32, and grow [T][KC] = the
+// slot-space row of each kept choice (-1 if dropped). The dx kernel below reads both
+// instead of recomputing the softmax in every h slice.
+template <int EP, int KC>
+__global__ void __launch_bounds__(256)
+    gate_dl_kernel(const float* __restrict__ logits, const int32_t* __restrict__ expert,
+                   const int32_t* __restrict__ slot, const float* __restrict__ prob, const float* __restrict__ dp,
+                   SlotSpace ss, int64_t T, float* __restrict__ dl_out, int32_t* __restrict__ grow,
+                   const float* __restrict__ aux_f, float aux_scale) {
+  constexpr int JL = EP > 32 ? 2 : 1;  // experts per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = ss.E;
+  const int64_t t = (int64_t)blockIdx.x * 8 + warp;
+  if (t >= T) return;
+  const float* lg = logits + (size_t)t * E;
+  float l[JL], m = -3.402823e38f;
+#pragma unroll
+  for (int i = 0; i < JL; ++i) {
+    const int j = lane + 32 * i;
+    l[i] = j < E ? lg[j] : -3.402823e38f;
+    m = fmaxf(m, l[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float ex[JL], den = 0.f;
+#pragma unroll
+  for (int i = 0; i < JL; ++i) {
+    ex[i] = lane + 32 * i < E ? expf(l[i] - m) : 0.f;
+    den += ex[i];
+  }
+  den = warp_sum(den);
+  const float inv = 1.f / den;
+  float fs = 0.f;  // sum_e f_e s_te (aux loss)
+  if (aux_f) {
+#pragma unroll
+    for (int i = 0; i < JL; ++i)
+      if (lane + 32 * i < E) fs += aux_f[lane + 32 * i] * (ex[i] * inv);
+    fs = warp_sum(fs);
+  }
+  float c1, c2 = 0.f;
+  int e1, e2 = -1;
+  if (KC == 2) {
+    // dL/ds_e1 = s2 (dw1 - dw2) / S^2, dL/ds_e2 = s1 (dw2 - dw1) / S^2 (dw = dp, 0 if dropped)
+    e1 = expert[2 * t];
+    e2 = expert[2 * t + 1];
+    const float s1 = expf(lg[e1] - m) * inv, s2 = expf(lg[e2] - m) * inv;
+    const float S = s1 + s2, dw1 = dp[2 * t], dw2 = dp[2 * t + 1];
+    c1 = s1 * s2 * (dw1 - dw2) / (S * S);
+    c2 = s2 * s1 * (dw2 - dw1) / (S * S);
+  } else {
+    e1 = expert[t];
+    c1 = slot[t] >= 0 ? dp[t] * prob[t] : 0.f;  // dropped: only the aux term
+  }
+#pragma unroll
+  for (int i = 0; i < JL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < E) {
+      const float sj = ex[i] * inv;
+      float v = c1 * ((j == e1 ? 1.f : 0.f) - sj);
+      if (KC == 2) v += c2 * ((j == e2 ? 1.f : 0.f) - sj);
+      if (aux_f) v += aux_scale * sj * (aux_f[j] - fs);
+      dl_out[(size_t)t * E + j] = v;
+    }
+  }
+  if (lane < KC) {
+    const int sl = slot[t * KC + lane];
+    int32_t r = -1;
+    if (sl >= 0) {
+      const int64_t tt = sl / ss.Cs, cs = sl - tt * ss.Cs;
+      r = (int32_t)((tt * E + expert[t * KC + lane]) * ss.Cs + cs);
+    }
+    grow[t * KC + lane] = r;
+  }
+}
+
 // ------------------------------------------------------------------ dx (+ dl)
 // CTA = 4 warps; warp w owns one m-tile of 16 tokens. It builds the A' fragments
 // of its tokens (softmax recomputed from the saved logits; lane 4g+tig covers
@@ -62,14 +136,10 @@ constexpr int DX_WARPS = 4;
 template <int EPK, int KC>
 __global__ void __launch_bounds__(DX_WARPS * 32)
     gate_bwd_dx_mma_kernel(const bf16* __restrict__ dS, const uint32_t* __restrict__ wpk,
-                           const float* __restrict__ logits, const int32_t* __restrict__ expert,
-                           const int32_t* __restrict__ slot, const float* __restrict__ prob,
-                           const float* __restrict__ dp, SlotSpace ss, int64_t T,
-                           bf16* __restrict__ dx, float* __restrict__ dl_out,
-                           const float* __restrict__ aux_f, float aux_scale) {
+                           const float* __restrict__ dl, const int32_t* __restrict__ grow, SlotSpace ss,
+                           int64_t T, bf16* __restrict__ dx, bool aux) {
   constexpr int KK = EPK / 16;  // k-steps per block of A'
   constexpr int KS = 3 * KK;
-  const bool aux = aux_f != nullptr;  // + d l_aux / d l for every token (R21)
   __shared__ __align__(16) float stage[DX_WARPS][16][64 + 4];
   extern __shared__ __align__(16) uint32_t wsm[];  // this CTA's B' fragments
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -95,74 +165,14 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int64_t t = t0 + g + 8 * half;
-    const int s = t < T ? slot[t * KC] : -1;
-    float dlv[KK][4];  // j = 16 kk + 2 tig + {0, 1, 8, 9}
+    float dlv[KK][4];  // j = 16 kk + 2 tig + {0, 1, 8, 9}, from gate_dl_kernel
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) dlv[kk][q] = 0.f;
-    if (KC == 2 && t < T) {
-      // dL/ds_e1 = s2 (dw1 - dw2) / S^2, dL/ds_e2 = s1 (dw2 - dw1) / S^2 (dw = dp, 0 if dropped)
-      const int e1 = expert[2 * t], e2 = expert[2 * t + 1];
-      const float* lg = logits + (size_t)t * E;
-      float m = -3.402823e38f;
-      for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
-      float den = 0.f;
-      for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
-      const float inv = 1.f / den;
-      const float s1 = expf(lg[e1] - m) * inv, s2 = expf(lg[e2] - m) * inv;
-      const float S = s1 + s2, dw1 = dp[2 * t], dw2 = dp[2 * t + 1];
-      const float c1 = s1 * s2 * (dw1 - dw2) / (S * S);  // g1 * s1
-      const float c2 = s2 * s1 * (dw2 - dw1) / (S * S);  // g2 * s2
-      float fs = 0.f;
-      if (aux)
-        for (int j = 0; j < E; ++j) fs += aux_f[j] * (expf(lg[j] - m) * inv);
-#pragma unroll
-      for (int kk = 0; kk < KK; ++kk)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
-          if (j < E) {
-            const float sj = expf(lg[j] - m) * inv;
-            float v = c1 * ((j == e1 ? 1.f : 0.f) - sj) + c2 * ((j == e2 ? 1.f : 0.f) - sj);
-            if (aux) v += aux_scale * sj * (aux_f[j] - fs);
-            dlv[kk][q] = v;
-          }
-        }
-    } else if (KC == 1 && t < T && (s >= 0 || aux)) {
-      const int e = expert[t];
-      const float* lg = logits + (size_t)t * E;
-      float m = -3.402823e38f;
-      for (int j = 0; j < E; ++j) m = fmaxf(m, lg[j]);
-      float den = 0.f;
-      for (int j = 0; j < E; ++j) den += expf(lg[j] - m);
-      const float gsc = s >= 0 ? dp[t] * prob[t] : 0.f;
-      const float inv = 1.f / den;
-      float fs = 0.f;  // sum_e f_e s_te
-      if (aux)
-        for (int j = 0; j < E; ++j) fs += aux_f[j] * (expf(lg[j] - m) * inv);
-#pragma unroll
-      for (int kk = 0; kk < KK; ++kk)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
-          if (j < E) {
-            const float sj = expf(lg[j] - m) * inv;
-            float v = gsc * ((j == e ? 1.f : 0.f) - sj);
-            if (aux) v += aux_scale * sj * (aux_f[j] - fs);
-            dlv[kk][q] = v;
-          }
-        }
-    }
-    if (t < T && blockIdx.y == 0) {
-#pragma unroll
-      for (int kk = 0; kk < KK; ++kk)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
-          if (j < E) dl_out[(size_t)t * E + j] = dlv[kk][q];
-        }
-    }
+      for (int q = 0; q < 4; ++q) {
+        const int j = 16 * kk + 2 * tig + (q & 1) + 8 * (q >> 1);
+        dlv[kk][q] = (t < T && j < E) ? __ldg(dl + (size_t)t * E + j) : 0.f;
+      }
     // A' fragments: a0/a2 rows g (half 0), a1/a3 rows g+8 (half 1)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -187,9 +197,9 @@ __global__ void __launch_bounds__(DX_WARPS * 32)
     valid[k] = t < T;
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
-      const int s = valid[k] ? slot[t * KC + c] : -1;
-      kept[k][c] = s >= 0;
-      rowoff[k][c] = kept[k][c] ? slot_row2(ss, expert[t * KC + c], s) : 0;
+      const int32_t gr = valid[k] ? __ldg(grow + t * KC + c) : -1;
+      kept[k][c] = gr >= 0;
+      rowoff[k][c] = kept[k][c] ? (size_t)gr * H : 0;
     }
   }
 
@@ -716,7 +726,7 @@ cudaError_t dwg_only(const void* x, const float* dl, int64_t T, int H, int E, fl
 template <int EPK, int EP, int KC>
 cudaError_t run(const void* x, const void* dS, const float* wg, const float* logits,
                 const int32_t* expert, const int32_t* slot, const float* prob, const float* dp,
-                const SlotSpace& ss, int64_t T, void* dx, float* dwg, float* dl, float* partial,
+                const SlotSpace& ss, int64_t T, void* dx, float* dwg, float* dl, int32_t* grow, float* partial,
                 int nsplit, uint32_t* wpk, const float* aux_f, float aux_scale, cudaStream_t s) {
   const int H = ss.H, E = ss.E;
   const int KS = 3 * EPK / 16;
@@ -726,9 +736,11 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   // split H so that the CTA's B' slice (per * KS * 256 bytes) stays small: more CTAs
   // (warps) per SM for this latency-bound gather + tiny-K MMA pass
   const int ntiles = H / 8;
+  // measured (emulated EP2 / TP2xEP2, ncu): 48 KiB for E <= 16 (53 vs 57 us at 1.3B),
+  // 96 KiB above (76 vs 79 us at 2.7B)
   static const int budget = [] {
     const char* e = getenv("MOE_DX_BUDGET_KB");  // development knob
-    return (e ? atoi(e) : 96) * 1024;
+    return (e ? atoi(e) : (EPK == 16 ? 48 : 96)) * 1024;
   }();
   int hsplit = 1;
   auto slice_bytes = [&](int hs) { return (size_t)(((ntiles + hs - 1) / hs + 7) & ~7) * KS * 256; };
@@ -749,9 +761,10 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   int64_t gx = (T + tb - 1) / tb;
   const int64_t cap = ((int64_t)per_sm * sms + hsplit - 1) / hsplit;  // one resident wave, persistent
   if (gx > cap) gx = cap;
+  gate_dl_kernel<EPK, KC><<<(unsigned)((T + 7) / 8), 256, 0, s>>>(logits, expert, slot, prob, dp, ss, T, dl, grow,
+                                                                  aux_f, aux_scale);
   gate_bwd_dx_mma_kernel<EPK, KC><<<dim3((unsigned)gx, hsplit), DX_WARPS * 32, smem, s>>>(
-      static_cast<const bf16*>(dS), wpk, logits, expert, slot, prob, dp, ss, T,
-      static_cast<bf16*>(dx), dl, aux_f, aux_scale);
+      static_cast<const bf16*>(dS), wpk, dl, grow, ss, T, static_cast<bf16*>(dx), aux_f != nullptr);
   constexpr int NT = EP <= 32 ? 4 : 2;
   constexpr int HB = 8 * NT * 8;
   const int64_t tps = ((T + nsplit - 1) / nsplit + DW_TT - 1) / DW_TT * DW_TT;
@@ -772,16 +785,16 @@ size_t gate_bwd_pack_bytes(int H, int E) {
 cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float* logits,
                      const int32_t* expert, const int32_t* slot, const float* prob,
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
-                     float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
+                     float* dl_scratch, int32_t* grow, float* dwg_partial, int nsplit, void* pack_scratch,
                      const float* aux_f, float aux_coef, cudaStream_t s) {
   if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * ss.H * ss.E, s);
   uint32_t* wpk = static_cast<uint32_t*>(pack_scratch);
   // d l_aux / d l_tj = coef * E / T * s_tj (f_j - sum_e f_e s_te)
   const float aux_scale = aux_f ? (float)((double)aux_coef * ss.E / (double)T) : 0.f;
 #define RUN(EPK, EP)                                                                                         \
-  (ss.K == 2 ? run<EPK, EP, 2>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch,        \
+  (ss.K == 2 ? run<EPK, EP, 2>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, grow,  \
                                dwg_partial, nsplit, wpk, aux_f, aux_scale, s)                                 \
-             : run<EPK, EP, 1>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch,        \
+             : run<EPK, EP, 1>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, grow,  \
                                dwg_partial, nsplit, wpk, aux_f, aux_scale, s))
   if (ss.E <= 8) return RUN(16, 8);  // EP >= 8: a lo row sits in the same thread as its hi row
   if (ss.E <= 16) return RUN(16, 16);

@@ -126,12 +126,13 @@ cudaError_t combine_bwd(const void* dy, const void* O, const int32_t* expert, co
 
 // B10: dx_t = dS[row(t)] + sum_j dl_tj Wg[:, j] (kept), 0 (dropped);
 // dl_tj = dp_t p_t (delta_{j,e*} - softmax(l_t)_j); dWg = sum_t x_t^T dl_t.
-// (gate_bwd.cu) warp-MMA implementation; pack_scratch holds gate_bwd_pack_bytes(H, E).
+// (gate_bwd.cu) dl and the gathered slot-space rows grow [T][K] in a token-parallel pre-pass,
+// dx by warp MMA; pack_scratch holds gate_bwd_pack_bytes(H, E).
 // aux_f: f_e [E] of the aux loss (R21) and its coefficient, or null / 0.
 cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float* logits,
                      const int32_t* expert, const int32_t* slot, const float* prob,
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
-                     float* dl_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
+                     float* dl_scratch, int32_t* grow_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
                      const float* aux_f, float aux_coef, cudaStream_t s);
 int gate_bwd_splits(int64_t T);
 // One-GPU top-1 (E <= 16) head of the backward in one launch: B1 (dp, dO incl. empty-slot
