@@ -1272,11 +1272,12 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     CUDA_TRY(c, gate_dwg_tc(X, at<uint8_t>(c->scratch, sc.aext), (int64_t)d.E * d.C, d.H, d.E, dwg,
                             at<float>(c->scratch, sc.dwgp), DWG_TC_SPLITS, at<int32_t>(c->scratch, sc.dwgc), st));
   } else {
-    Scope sc_(c, MOE_K_GATE_BWD, st, 5);
+    Scope sc_(c, MOE_K_GATE_BWD, st, d.E <= 32 ? 4 : 5);
     CUDA_TRY(c, gate_bwd(x, dS, wg, logits, expert, slot, prob, dp, ss, d.T, dx, dwg,
                          at<float>(c->scratch, sc.dl), at<int32_t>(c->scratch, sc.grow),
                          at<float>(c->scratch, sc.dwgp), sc.nsplit,
-                         at<uint8_t>(c->scratch, sc.wpk),
+                         at<uint8_t>(c->scratch, sc.wpk), at<uint8_t>(c->scratch, sc.atok),
+                         at<int32_t>(c->scratch, sc.dwgc),
                          d.aux ? at<const float>(saved, sv.aux) : nullptr, d.aux_coef, st));
   }
   c->last_stream = st;

@@ -56,11 +56,13 @@ __global__ void __launch_bounds__(256)
     gate_dl_kernel(const float* __restrict__ logits, const int32_t* __restrict__ expert,
                    const int32_t* __restrict__ slot, const float* __restrict__ prob, const float* __restrict__ dp,
                    SlotSpace ss, int64_t T, float* __restrict__ dl_out, int32_t* __restrict__ grow,
-                   const float* __restrict__ aux_f, float aux_scale) {
+                   const float* __restrict__ aux_f, float aux_scale, bf16* __restrict__ a_tok,
+                   int32_t* __restrict__ dwg_cnt, int ncnt) {
   constexpr int JL = EP > 32 ? 2 : 1;  // experts per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int E = ss.E;
   const int64_t t = (int64_t)blockIdx.x * 8 + warp;
+  if (a_tok && blockIdx.x == 0 && threadIdx.x < ncnt) dwg_cnt[threadIdx.x] = 0;  // dwg_tc's split counters
   if (t >= T) return;
   const float* lg = logits + (size_t)t * E;
   float l[JL], m = -3.402823e38f;
@@ -111,6 +113,20 @@ __global__ void __launch_bounds__(256)
       if (aux_f) v += aux_scale * sj * (aux_f[j] - fs);
       dl_out[(size_t)t * E + j] = v;
     }
+  }
+  if (EP <= 32 && a_tok) {
+    // dwg_tc's B operand, token order: [hi(dl) | lo(dl) | 0] (EP columns per block, 64 wide)
+    const int j = lane;
+    float v = 0.f;
+    if (j < E) v = dl_out[(size_t)t * E + j];
+    bf16 hi, lo;
+    split_bf16(v, hi, lo);
+    bf16* ar = a_tok + (size_t)t * 64;
+    if (j < EP) {
+      ar[j] = hi;
+      ar[EP + j] = lo;
+    }
+    if (2 * EP + j < 64) ar[2 * EP + j] = __float2bfloat16_rn(0.f);
   }
   if (lane < KC) {
     const int sl = slot[t * KC + lane];
@@ -554,6 +570,15 @@ constexpr int STAGES = 8;
 constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
 constexpr int THREADS = 192;
 
+__device__ __forceinline__ void tmem_ld16(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta));
+}
+
 __device__ __forceinline__ uint64_t mn_desc(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
@@ -564,6 +589,7 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t addr) {
   return d;
 }
 
+template <int EP>
 __global__ void __launch_bounds__(THREADS, 1)
     dwg_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t rows,
                   int H, int E, int mtiles, int nsplit, float* __restrict__ partial, int32_t* __restrict__ cnt,
@@ -639,41 +665,34 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
   } else {
-    // epilogue warps 0-3: TMEM lane = h row of the tile
+    // epilogue warps 0-3: TMEM lane = h row of the tile; dWg[h][j] = D[h][j] + D[h][EP + j]
+    // (a_ext columns [hi(dl) | lo(dl)], EP = 16 or 32)
     const int hl = warp * 32 + lane;
     const int h = h0 + hl;
-    float v[16];
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
     if (nkb > 0) {
       mbar_wait(smem_u32(&bars[2 * STAGES]), 0);
       tc_fence_after();
-      uint32_t hi[16], lo[16];
-      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-          : "=r"(hi[0]), "=r"(hi[1]), "=r"(hi[2]), "=r"(hi[3]), "=r"(hi[4]), "=r"(hi[5]), "=r"(hi[6]),
-            "=r"(hi[7]), "=r"(hi[8]), "=r"(hi[9]), "=r"(hi[10]), "=r"(hi[11]), "=r"(hi[12]), "=r"(hi[13]),
-            "=r"(hi[14]), "=r"(hi[15])
-          : "r"(ta));
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-          : "=r"(lo[0]), "=r"(lo[1]), "=r"(lo[2]), "=r"(lo[3]), "=r"(lo[4]), "=r"(lo[5]), "=r"(lo[6]),
-            "=r"(lo[7]), "=r"(lo[8]), "=r"(lo[9]), "=r"(lo[10]), "=r"(lo[11]), "=r"(lo[12]), "=r"(lo[13]),
-            "=r"(lo[14]), "=r"(lo[15])
-          : "r"(ta + 16));
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(hi[j]) + __uint_as_float(lo[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = 0.f;
     }
-    if (h < H) {
-      float* prow = partial + ((size_t)split * H + h) * E;
+    float* prow = partial + ((size_t)split * H + (h < H ? h : 0)) * E;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < E) prow[j] = v[j];
+    for (int c = 0; c < EP; c += 16) {
+      float v[16];
+      if (nkb > 0) {
+        uint32_t hi[16], lo[16];
+        tmem_ld16(ta + c, hi);
+        tmem_ld16(ta + EP + c, lo);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(hi[j]) + __uint_as_float(lo[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      }
+      if (h < H)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c + j < E) prow[c + j] = v[j];
     }
     __threadfence();
     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -684,18 +703,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (h < H) {
         // sum over splits in split order per j; the loads of several splits are issued
         // together (a load -> add chain per (j, split) made this tail ~half the kernel)
-        float acc[16];
+        float acc[EP];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+        for (int j = 0; j < EP; ++j) acc[j] = 0.f;
 #pragma unroll 4
         for (int sp = 0; sp < nsplit; ++sp) {
           const float* pr = partial + ((size_t)sp * H + h) * E;
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
+          for (int j = 0; j < EP; ++j)
             if (j < E) acc[j] += __ldcg(pr + j);
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < EP; ++j)
           if (j < E) dwg[(size_t)h * E + j] = acc[j];
       }
       if (threadIdx.x == 0) cnt[mt] = 0;
@@ -727,7 +746,8 @@ template <int EPK, int EP, int KC>
 cudaError_t run(const void* x, const void* dS, const float* wg, const float* logits,
                 const int32_t* expert, const int32_t* slot, const float* prob, const float* dp,
                 const SlotSpace& ss, int64_t T, void* dx, float* dwg, float* dl, int32_t* grow, float* partial,
-                int nsplit, uint32_t* wpk, const float* aux_f, float aux_scale, cudaStream_t s) {
+                int nsplit, uint32_t* wpk, void* a_tok_scratch, int32_t* dwg_cnt, const float* aux_f, float aux_scale,
+                cudaStream_t s) {
   const int H = ss.H, E = ss.E;
   const int KS = 3 * EPK / 16;
   const int64_t npack = (int64_t)(H / 8) * KS * 32;
@@ -761,10 +781,13 @@ cudaError_t run(const void* x, const void* dS, const float* wg, const float* log
   int64_t gx = (T + tb - 1) / tb;
   const int64_t cap = ((int64_t)per_sm * sms + hsplit - 1) / hsplit;  // one resident wave, persistent
   if (gx > cap) gx = cap;
+  bf16* a_tok = EPK <= 32 ? static_cast<bf16*>(a_tok_scratch) : nullptr;
   gate_dl_kernel<EPK, KC><<<(unsigned)((T + 7) / 8), 256, 0, s>>>(logits, expert, slot, prob, dp, ss, T, dl, grow,
-                                                                  aux_f, aux_scale);
+                                                                  aux_f, aux_scale, a_tok, dwg_cnt, (H + 127) / 128);
   gate_bwd_dx_mma_kernel<EPK, KC><<<dim3((unsigned)gx, hsplit), DX_WARPS * 32, smem, s>>>(
       static_cast<const bf16*>(dS), wpk, dl, grow, ss, T, static_cast<bf16*>(dx), aux_f != nullptr);
+  if (EPK <= 32)  // dWg on the tensor cores from the token-order [hi | lo](dl) rows (one launch)
+    return gate_dwg_tc(x, a_tok, T, H, E, dwg, partial, DWG_TC_SPLITS, dwg_cnt, s);
   constexpr int NT = EP <= 32 ? 4 : 2;
   constexpr int HB = 8 * NT * 8;
   const int64_t tps = ((T + nsplit - 1) / nsplit + DW_TT - 1) / DW_TT * DW_TT;
@@ -786,6 +809,7 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      const int32_t* expert, const int32_t* slot, const float* prob,
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                      float* dl_scratch, int32_t* grow, float* dwg_partial, int nsplit, void* pack_scratch,
+                     void* a_tok_scratch, int32_t* dwg_cnt,
                      const float* aux_f, float aux_coef, cudaStream_t s) {
   if (T <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * ss.H * ss.E, s);
   uint32_t* wpk = static_cast<uint32_t*>(pack_scratch);
@@ -793,9 +817,9 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
   const float aux_scale = aux_f ? (float)((double)aux_coef * ss.E / (double)T) : 0.f;
 #define RUN(EPK, EP)                                                                                         \
   (ss.K == 2 ? run<EPK, EP, 2>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, grow,  \
-                               dwg_partial, nsplit, wpk, aux_f, aux_scale, s)                                 \
+                               dwg_partial, nsplit, wpk, a_tok_scratch, dwg_cnt, aux_f, aux_scale, s)                                 \
              : run<EPK, EP, 1>(x, dS, wg, logits, expert, slot, prob, dp, ss, T, dx, dwg, dl_scratch, grow,  \
-                               dwg_partial, nsplit, wpk, aux_f, aux_scale, s))
+                               dwg_partial, nsplit, wpk, a_tok_scratch, dwg_cnt, aux_f, aux_scale, s))
   if (ss.E <= 8) return RUN(16, 8);  // EP >= 8: a lo row sits in the same thread as its hi row
   if (ss.E <= 16) return RUN(16, 16);
   if (ss.E <= 32) return RUN(32, 32);
@@ -817,10 +841,9 @@ cudaError_t combine_bwd_gate(const void* dy, const void* O, const int32_t* exper
   return cudaGetLastError();
 }
 
-cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, int E, float* dwg, float* partial,
-                        int max_split, int32_t* counters, cudaStream_t s) {
-  if (E > 16) return cudaErrorInvalidValue;
-  if (rows <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * H * E, s);
+template <int EP>
+static cudaError_t dwg_tc_launch(const void* X, const void* a_ext, int64_t rows, int H, int E, float* dwg,
+                                 float* partial, int max_split, int32_t* counters, cudaStream_t s) {
   CUtensorMap ta, tb;
   int sms = 0;
   cudaError_t e = tensor_map_bf16(&ta, X, (uint64_t)H, (uint64_t)rows, 64, 64, &sms);
@@ -828,7 +851,7 @@ cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, i
   if (e != cudaSuccess) return e;
   static std::atomic<bool> attr{false};  // idempotent; ranks may launch from several threads
   if (!attr) {
-    e = cudaFuncSetAttribute(dwtc::dwg_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dwtc::SMEM);
+    e = cudaFuncSetAttribute(dwtc::dwg_tc_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dwtc::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -843,12 +866,21 @@ cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, i
   cfg.blockDim = dim3(dwtc::THREADS);
   cfg.dynamicSmemBytes = dwtc::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];  // the prologue overlaps the tail of the weight-gradient GEMM
+  cudaLaunchAttribute at[1];  // the prologue overlaps the tail of the previous kernel
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dwtc::dwg_tc_kernel, ta, tb, rows, H, E, mtiles, nsplit, partial, counters, dwg);
+  return cudaLaunchKernelEx(&cfg, dwtc::dwg_tc_kernel<EP>, ta, tb, rows, H, E, mtiles, nsplit, partial, counters,
+                            dwg);
+}
+
+cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, int E, float* dwg, float* partial,
+                        int max_split, int32_t* counters, cudaStream_t s) {
+  if (E > 32) return cudaErrorInvalidValue;
+  if (rows <= 0) return cudaMemsetAsync(dwg, 0, sizeof(float) * H * E, s);
+  return E <= 16 ? dwg_tc_launch<16>(X, a_ext, rows, H, E, dwg, partial, max_split, counters, s)
+                 : dwg_tc_launch<32>(X, a_ext, rows, H, E, dwg, partial, max_split, counters, s);
 }
 
 cudaError_t gate_dwg(const void* x, const float* dl, int64_t T, int H, int E, float* dwg, float* partial,

@@ -133,6 +133,7 @@ cudaError_t gate_bwd(const void* x, const void* dS, const float* wg, const float
                      const int32_t* expert, const int32_t* slot, const float* prob,
                      const float* dp, const SlotSpace& ss, int64_t T, void* dx, float* dwg,
                      float* dl_scratch, int32_t* grow_scratch, float* dwg_partial, int nsplit, void* pack_scratch,
+                     void* a_tok_scratch, int32_t* dwg_counters,
                      const float* aux_f, float aux_coef, cudaStream_t s);
 int gate_bwd_splits(int64_t T);
 // One-GPU top-1 (E <= 16) head of the backward in one launch: B1 (dp, dO incl. empty-slot
@@ -143,8 +144,9 @@ cudaError_t combine_bwd_gate(const void* dy, const void* O, const int32_t* exper
                              const int32_t* count, const float* wg, int64_t T, int H, int E, int64_t C,
                              void* dO, float* dl, void* a_ext, void* b_ext, void* dx, int32_t* dwg_cnt,
                              cudaStream_t s);
-// dWg on the tensor cores from the dispatched rows X [rows][H] and the K-extension rows
-// a_ext [rows][64] (one GPU, top-1, E <= 16): one launch, split-K partials [<= max_split][H][E]
+// dWg on the tensor cores from rows X [rows][H] and rows a_ext [rows][64] = [hi(dl) | lo(dl) | ...]
+// (EP = 16 or 32 columns per block; one GPU: the dispatched rows and the K-extension rows,
+// E <= 16; general B10 path: the token rows and [hi | lo](dl), E <= 32): one launch, split-K partials [<= max_split][H][E]
 // summed in fixed order by the last CTA of each h tile; counters [ceil(H/128)] zeroed by
 // combine_bwd_gate.
 cudaError_t gate_dwg_tc(const void* X, const void* a_ext, int64_t rows, int H, int E, float* dwg, float* partial,

@@ -144,6 +144,7 @@ void make_layouts(const Dims& d, SavedLayout* sv, ScratchLayout* sc) {
   sc->dp = b.take((size_t)d.T * d.K * 4);
   sc->dl = b.take((size_t)d.T * d.E * 4);
   sc->grow = b.take((size_t)d.T * d.K * 4);  // gathered slot-space rows of the general B10
+  sc->atok = b.take((size_t)d.T * 64 * 2);     // its [hi | lo](dl) rows for the tcgen05 dWg
   sc->dwgp = b.take((size_t)(sc->nsplit > DWG_TC_SPLITS ? sc->nsplit : DWG_TC_SPLITS) * d.H * d.E * 4);
   sc->dwgc = b.take((size_t)((d.H + 127) / 128) * 4);  // split-K counters of the one-GPU dWg launch
   sc->wpk = b.take(gate_bwd_pack_bytes(d.H, d.E));

@@ -47,7 +47,7 @@ struct ScratchLayout {
   // forward
   size_t local_rank, block_hist, tile_ties, auxp, D, Ypart;
   // backward
-  size_t dp, dl, grow, dwgp, dwgc, wpk, dO, dY, dH, dXp, dS, aext, bext;
+  size_t dp, dl, grow, atok, dwgp, dwgc, wpk, dO, dY, dH, dXp, dS, aext, bext;
   // checkpoint mode: G, A re-materialized by the replay (outside both regions)
   size_t Grec, Arec;
   size_t total;
