@@ -757,8 +757,10 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[2], c->side));
     Scope sc_(c, MOE_K_COMM, st, 0);
-    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[2], 0));
+    // the own pieces (SM copy) need only GEMM2's output: they overlap the side stream's
+    // last copy-engine pieces instead of following them
     TRY(exchange_local(c, Y, c->comm->wo(rslot), st));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[2], 0));
     TRY(barrier(c, st));
     if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
     if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
@@ -1246,8 +1248,8 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
       TRY(gemm(c, g7, st));
     }
     Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(exchange_local(c, dXp, moe_comm::W_DS, st));  // own pieces: need only B5's output
     CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[1], 0));
-    TRY(exchange_local(c, dXp, moe_comm::W_DS, st));
     TRY(barrier(c, st));
     if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
     if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
