@@ -46,6 +46,7 @@ struct moe_ctx {
   bool no_fused_dx = false;    // MOE_NO_FUSED_DX=1: B10 as a separate kernel (A/B, tests)
   bool no_fused_combine = false;  // MOE_NO_FUSED_COMBINE=1: F11 as a separate kernel
   bool no_gemm_signal = false;    // MOE_NO_GEMM_SIGNAL=1: GEMM2 parts as separate launches (A/B)
+  bool no_fused_return = false;   // MOE_NO_FUSED_RETURN=1: F9 by copy engines after GEMM2 parts (A/B)
   moe_stats stats;
   std::unordered_set<const void*> saved_written;
   // peer-memory exchange (d.peer): this layer's piece lists over the comm's windows
@@ -707,6 +708,29 @@ moe_status forward_core(moe_ctx* c, const void* x, const void* w1, const void* w
       CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.O), O, (size_t)d.E * d.C * d.H * 2,
                                   cudaMemcpyDeviceToDevice, st));
     }
+  } else if (d.peer && split && !c->no_fused_return) {
+    // (G_t = 1, split exchange) F7 + F9 fused: GEMM2's epilogue stores every row straight
+    // into the slot-space window of its source rank over peer memory (the own rows into the
+    // own window), so the return all-to-all overlaps the math tile by tile and needs no
+    // copy engines, part launches or staging; one barrier publishes the windows.
+    GemmArgs g2{d.El, (int)d.R, d.H, d.Fl, A, 0, w2, 0, Y, EPI_STORE, nullptr};
+    PeerOut po;
+    po.table = c->comm->d_table;
+    po.nwin = c->comm->nwin;
+    po.win = c->comm->wo(rslot);
+    po.rank0 = d.d * d.Gep;  // G_t = 1: rank = d * G_ep + ep
+    po.e0 = d.ep * d.El;
+    po.C = d.C;
+    g2.po = &po;
+    TRY(gemm(c, g2, st));
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(barrier(c, st));
+    if (d.Gep > 1) ledger(c, MOE_COLL_A2A, pass, c->ret_bytes[1]);
+    if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, pass, c->ret_bytes[2]);
+    if (d.ckpt) {  // CAC stash of the second collective's output
+      CUDA_TRY(c, cudaMemcpyAsync(at<uint8_t>(saved, sv.O), O, (size_t)d.E * d.C * d.H * 2,
+                                  cudaMemcpyDeviceToDevice, st));
+    }
   } else if (d.peer) {
     // (G_t = 1) F7 GEMM2 in up to 4 expert parts; each part's return pieces (F9) go out on
     // the side stream (copy engines) while the next part computes, so only the last part's
@@ -888,6 +912,8 @@ moe_status make_ctx(const moe_config* cfg, moe_comm* m, int world, int rank, voi
     c->overlap = !(no && no[0] == '1');
     const char* ns = std::getenv("MOE_NO_GEMM_SIGNAL");
     c->no_gemm_signal = ns && ns[0] == '1';
+    const char* nr = std::getenv("MOE_NO_FUSED_RETURN");
+    c->no_fused_return = nr && nr[0] == '1';
   }
   c->d = d;
   c->cfg = *cfg;
@@ -1193,10 +1219,30 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
     g5.epilogue = EPI_SCATTER;
     g5.gdx = &gdx;
   }
+  // (G_t = 1, split exchange) B5 + B8 fused: dX rows straight into the source ranks' dS
+  // windows from B5's epilogue (as F7 + F9 in the forward)
+  const bool fused_ret = split && !c->no_fused_return;
+  PeerOut po;
+  if (fused_ret) {
+    po.table = c->comm->d_table;
+    po.nwin = c->comm->nwin;
+    po.win = moe_comm::W_DS;
+    po.rank0 = d.d * d.Gep;
+    po.e0 = d.ep * d.El;
+    po.C = d.C;
+    g5.po = &po;
+  }
   TRY(gemm(c, g5, st));
   GemmArgs g6{d.El, d.H, d.Fl, (int)d.R, dY, 1, A, 1, dw2, EPI_STORE, nullptr};
   GemmArgs g7{d.El, d.Fl, d.H, (int)d.R, dH, 1, X, 1, dw1, EPI_STORE, nullptr};
-  if (d.peer && d.Gt > 1) {
+  if (fused_ret) {
+    TRY(gemm(c, g6, st));
+    TRY(gemm(c, g7, st));
+    Scope sc_(c, MOE_K_COMM, st, 0);
+    TRY(barrier(c, st));  // every rank's B5 rows are in the dS windows
+    if (d.Gep > 1) ledger(c, MOE_COLL_A2A, 1, c->ret_bytes[1]);
+    if (d.dtd) ledger(c, MOE_COLL_ALLGATHER, 1, c->ret_bytes[2]);
+  } else if (d.peer && d.Gt > 1) {
     // B7-B9 fused over peer memory (tp_return), then the weight-gradient GEMMs
     {
       Scope sc_(c, MOE_K_COMM, st, 0);

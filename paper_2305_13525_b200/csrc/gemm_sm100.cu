@@ -50,6 +50,7 @@ struct Params {
   bf16* aux;
   GateDxArgs g;  // EPI_SCATTER / EPI_COMBINE
   GemmSignal sig;  // sig.cnt != null: per-part completion flags (EPI_STORE)
+  PeerOut po;      // po.table != null: rows into the source ranks' windows (EPI_STORE)
 };
 
 // UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1.
@@ -344,7 +345,13 @@ __global__ void __launch_bounds__(threads2(EPI), 1)
             if (trow >= 0 && col_ok)
               st_v4(static_cast<bf16*>(p.g.dx) + (size_t)trow * p.N + n + qq * 8, vd);
           } else if (ok) {
-            st_v4(p.D + go, vd);
+            if (EPI == EPI_STORE && p.po.table) {  // F9 fused: the row goes to its source rank
+              const int64_t sblk = mm / p.po.C;
+              bf16* base = static_cast<bf16*>(p.po.table[(p.po.rank0 + sblk) * p.po.nwin + p.po.win]);
+              st_v4(base + ((size_t)(p.po.e0 + b) * p.po.C + (mm - sblk * p.po.C)) * p.N + n + qq * 8, vd);
+            } else {
+              st_v4(p.D + go, vd);
+            }
           }
           if (EPI == EPI_GELU) {
             const uint4 vx = ld_shared_v4(bX + off);
@@ -494,6 +501,14 @@ cudaError_t gemm_tc(const GemmArgs& a, cudaStream_t s, const char** why) {
   p.D = static_cast<bf16*>(a.D);
   p.aux = static_cast<bf16*>(a.aux);
   p.g = a.gdx ? *a.gdx : GateDxArgs{};
+  p.po = PeerOut{};
+  if (a.po) {
+    if (a.epilogue != EPI_STORE || a.a_bs || a.d_bs || a.po->C <= 0) {
+      *why = "fused return: plain epilogue, dense batches";
+      return cudaErrorNotSupported;
+    }
+    p.po = *a.po;
+  }
   p.sig = GemmSignal{};
   if (a.sig) {
     if (a.epilogue != EPI_STORE || a.sig->nparts < 1 || a.sig->nparts > 4 || a.sig->part_b[a.sig->nparts] != a.batch) {

@@ -43,6 +43,16 @@ struct GemmSignal {
   int part_b[5] = {0, 0, 0, 0, 0};
 };
 
+// Fused return exchange (G_t = 1 split mode, F7 -> F9): EPI_STORE rows of batch b (local
+// expert) go straight into the slot-space window of their source rank over peer memory:
+// row m of source block s = m / C lands at ((e0 + b) C + m - s C) of window `win` of rank
+// rank0 + s (table: [world][nwin] window pointers, device). The GEMM's D is not written.
+struct PeerOut {
+  void* const* table = nullptr;
+  int nwin = 0, win = 0, rank0 = 0, e0 = 0;
+  int64_t C = 0;
+};
+
 struct GemmArgs {
   int batch, M, N, K;
   const void* A;
@@ -58,6 +68,7 @@ struct GemmArgs {
   int64_t a_bs = 0, d_bs = 0;
   const GateDxArgs* gdx = nullptr;  // EPI_SCATTER / EPI_COMBINE only
   const GemmSignal* sig = nullptr;  // EPI_STORE only: per-part completion flags
+  const PeerOut* po = nullptr;      // EPI_STORE only: rows stored into the source ranks' windows
 };
 
 // tcgen05 / TMEM / TMA kernel (the product path).
