@@ -574,19 +574,30 @@ def main():
                "optimizer": optim}
         if world > 1:
             # a2a bandwidth: bytes this rank sends to other ranks per step. In peer
-            # mode every remote piece of a G_t = 1 layer travels on the copy engines (class "xfer",
-            # CUDA events on the side stream around the copies, overlapped with the GEMMs), so
-            # egress / xfer time is the link rate achieved; otherwise (fused SM stores / NCCL) the
-            # time basis is the kernel classes that move the bytes, a lower bound.
+            # mode with G_t = 1 the dispatch direction (X forward, dO backward: half of the a2a
+            # bytes) travels on the copy engines (class "xfer", CUDA events on the side stream
+            # around the copies, overlapped with the GEMMs) and the return direction is stored by
+            # the GEMM epilogues themselves (F7+F9, B5+B8), so the link rate is the dispatch
+            # bytes / xfer time; otherwise (fused SM stores / NCCL) the time basis is the kernel
+            # classes that move the bytes, a lower bound.
             wb = {k: v / args.steps for k, v in st["wire_bytes"].items()}
             egress = sum(wb.values())
             xfer_ms = per_class.get("xfer", 0.0)
+            fused_return = os.environ.get("MOE_NO_FUSED_RETURN", "0") != "1"
             if xfer_ms > 0 and gt == 1:
-                ex_ms, basis = xfer_ms, "copy-engine transfers (xfer class, side stream)"
+                ex_ms = xfer_ms
+                if fused_return:
+                    egress_rate = wb["a2a"] / 2
+                    basis = "dispatch-direction copy-engine transfers (xfer class) for half the a2a bytes; " \
+                            "the return half is stored by the GEMM epilogues"
+                else:
+                    egress_rate = egress
+                    basis = "copy-engine transfers (xfer class, side stream)"
+                gbs = egress_rate / (ex_ms / 1e3) / 1e9
             else:
                 ex_ms = per_class["comm"] + per_class["dispatch"] + per_class["combine_bwd"] + xfer_ms
                 basis = "comm + dispatch + combine_bwd + xfer classes (lower bound)"
-            gbs = egress / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None
+                gbs = egress / (ex_ms / 1e3) / 1e9 if ex_ms > 0 else None
             out["comm_ms_per_step"] = per_class["comm"]
             out["a2a"] = {"a2a_bytes_per_step": wb["a2a"], "egress_bytes_per_step": egress,
                           "transfer_ms_per_step": ex_ms, "egress_GB/s": gbs,
