@@ -70,6 +70,25 @@ def test_emulated_exchange_parity(gt, gep):
     print("max rel L2", {k: max(v for (r, n), v in errs.items() if n == k) for k in ("y", "dx", "dwg", "dw1", "dw2")})
 
 
+@pytest.mark.parametrize("gep", [2, 4])
+def test_emulated_return_paths_bitwise(gep, monkeypatch):
+    """G_t = 1 split exchange: the return all-to-all fused into the GEMM epilogues (F7+F9,
+    B5+B8 peer stores, the default) against the copy-engine return driven by GEMM2's
+    completion flags (MOE_NO_FUSED_RETURN=1) and against the per-part launches
+    (+ MOE_NO_GEMM_SIGNAL=1): where rows travel never changes their arithmetic, so all three
+    are bitwise equal, and the fused one matches the oracle."""
+    wl = emu.Workload(_shape(1, gep))
+    fused = emu.run_modes(wl, {"m": wl.config(True)})
+    fails = emu.oracle_failures(wl, fused, "m")[0]
+    monkeypatch.setenv("MOE_NO_FUSED_RETURN", "1")
+    ce = emu.run_modes(wl, {"m": wl.config(True)})
+    monkeypatch.setenv("MOE_NO_GEMM_SIGNAL", "1")
+    parts = emu.run_modes(wl, {"m": wl.config(True)})
+    for other in (ce, parts):
+        fails += emu.bitwise_failures([{"a": a["m"], "b": b["m"]} for a, b in zip(fused, other)], "a", "b")
+    assert not fails, "\n".join(fails[:40])
+
+
 @pytest.mark.parametrize("gt,gep", [(2, 2), (4, 1), (1, 4), (2, 4)])
 def test_emulated_drops(gt, gep):
     """cf 0.5 with an oversubscribed expert: DTD slices of partly empty capacity buffers."""
