@@ -1168,7 +1168,7 @@ moe_status moe_backward(moe_ctx* c, const void* dy, const void* saved, const voi
   if (split) {
     SplitDst sd{dY, dO, d.ep, d.El, d.Gep};
     {
-      Scope sc_(c, MOE_K_COMBINE_BWD, st, 2);
+      Scope sc_(c, MOE_K_COMBINE_BWD, st, 1);
       CUDA_TRY(c, combine_bwd_split(dy, O, expert, slot, prob, count, ss, d.T, dp, sd, st));
     }
     CUDA_TRY(c, cudaEventRecord(c->ev[3], st));

@@ -405,14 +405,23 @@ __global__ void __launch_bounds__(WARPS * 32)
   else copy_row<true>(nullptr, dst, nv, lane);
 }
 
+constexpr int SPLIT_ZW = 4;  // warps per expert zeroing its empty slot rows (combine_bwd_split)
 __global__ void __launch_bounds__(WARPS * 32)
     combine_bwd_split_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ O,
                              const int32_t* __restrict__ expert, const int32_t* __restrict__ slot,
                              const float* __restrict__ prob, SlotSpace ss, int64_t T,
-                             float* __restrict__ dp, SplitDst sd) {
+                             float* __restrict__ dp, SplitDst sd, const int32_t* __restrict__ count) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (t >= T) return;
+  if (t >= T) {
+    // trailing warps, SPLIT_ZW per expert: zero the empty slot rows [count_e, C)
+    const int64_t w = t - T;
+    if (w >= (int64_t)ss.E * SPLIT_ZW) return;
+    const int e = (int)(w / SPLIT_ZW), part = (int)(w % SPLIT_ZW);
+    for (int64_t c = count[e] + part; c < ss.C; c += SPLIT_ZW)
+      copy_row<true>(nullptr, split_row(sd, ss, e, c), ss.H / 8, lane);
+    return;
+  }
   for (int kc = 0; kc < ss.K; ++kc) {
     const int64_t it = t * ss.K + kc;
     const int s = slot[it];
@@ -457,16 +466,6 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 }
 
-__global__ void __launch_bounds__(WARPS * 32)
-    zero_empty_split_kernel(const int32_t* __restrict__ count, SlotSpace ss, int64_t rows, SplitDst sd) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (r >= rows) return;
-  const int e = (int)(r / ss.C);
-  const int64_t c = r % ss.C;
-  if (c < count[e]) return;
-  copy_row<true>(nullptr, split_row(sd, ss, e, c), ss.H / 8, lane);
-}
 
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + WARPS - 1) / WARPS); }
 
@@ -545,11 +544,12 @@ cudaError_t dispatch_split(const void* x, const int32_t* tok_of, const int32_t* 
 cudaError_t combine_bwd_split(const void* dy, const void* O, const int32_t* expert, const int32_t* slot,
                               const float* prob, const int32_t* count, const SlotSpace& ss, int64_t T,
                               float* dp, const SplitDst& sd, cudaStream_t s) {
-  if (T > 0)
-    combine_bwd_split_kernel<<<blocks_for(T), WARPS * 32, 0, s>>>(
-        static_cast<const bf16*>(dy), static_cast<const bf16*>(O), expert, slot, prob, ss, T, dp, sd);
-  const int64_t rows = (int64_t)ss.E * ss.C;
-  if (rows > 0) zero_empty_split_kernel<<<blocks_for(rows), WARPS * 32, 0, s>>>(count, ss, rows, sd);
+  // one launch: a warp per token (dp, dO rows of the kept choices) and SPLIT_ZW warps per
+  // expert zeroing its empty slot rows
+  const int64_t warps = T + (int64_t)ss.E * SPLIT_ZW;
+  if (warps > 0 && ss.C > 0)
+    combine_bwd_split_kernel<<<blocks_for(warps), WARPS * 32, 0, s>>>(
+        static_cast<const bf16*>(dy), static_cast<const bf16*>(O), expert, slot, prob, ss, T, dp, sd, count);
   return cudaGetLastError();
 }
 
